@@ -1,0 +1,111 @@
+"""CPU oracle for the SpMV hot path of arXiv 2212.08964 (ctypes wrapper over oracle.c).
+
+TEST INFRASTRUCTURE ONLY: tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` legs are the only callers.  It shares no code with the CUDA product
+(paper_2212_08964_b200/) and the product never imports it.
+
+Every function follows the plain definition of what the method computes (see oracle.c
+for the PAPER.md citations); pins live in tests/test_oracle_pins.py.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c with gcc (no fast-math, no FP contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
+                               "-shared", "-o", _LIB, _SRC])
+    return _LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        i64, p = ctypes.c_int64, ctypes.c_void_p
+        L.oracle_spmv.argtypes = [i64, p, p, p, p, p, p]
+        L.oracle_spmv_omp.argtypes = [i64, p, p, p, p, p, p]
+        L.oracle_spmv_packed.argtypes = [i64, p, p, p, p, p, p]
+        L.oracle_partition.argtypes = [i64, i64, p, i64, p]
+        L.oracle_partition.restype = i64
+        L.oracle_shard_bounds.argtypes = [i64, p, ctypes.c_int32, p]
+        L.oracle_num_threads.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _np(a, dtype):
+    """torch tensor / list / ndarray -> contiguous host ndarray of dtype."""
+    if hasattr(a, "detach"):
+        a = a.detach().cpu().numpy()
+    a = np.ascontiguousarray(np.asarray(a), dtype=dtype)
+    return a
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def spmv(row_offsets, col_idx, values, x, threads: bool = False):
+    """y = A x in double, plus s_i = sum_k |a_ik x_k|.  Returns (y, s) as float64 arrays."""
+    off = _np(row_offsets, np.int32)
+    col = _np(col_idx, np.int32)
+    val = _np(values, np.float32)
+    xx = _np(x, np.float32)
+    rows = off.size - 1
+    y = np.empty(rows, np.float64)
+    s = np.empty(rows, np.float64)
+    f = lib().oracle_spmv_omp if threads else lib().oracle_spmv
+    f(rows, _ptr(off), _ptr(col), _ptr(val), _ptr(xx), _ptr(y), _ptr(s))
+    return y, s
+
+
+def spmv_packed(sel_offsets, sel_cols, sel_vals, x):
+    """Definition of y on a packed subset of rows (for sampled parity at full size)."""
+    so = _np(sel_offsets, np.int64)
+    sc = _np(sel_cols, np.int32)
+    sv = _np(sel_vals, np.float32)
+    xx = _np(x, np.float32)
+    n = so.size - 1
+    y = np.empty(n, np.float64)
+    s = np.empty(n, np.float64)
+    lib().oracle_spmv_packed(n, _ptr(so), _ptr(sc), _ptr(sv), _ptr(xx), _ptr(y), _ptr(s))
+    return y, s
+
+
+def partition(row_offsets, L: int) -> np.ndarray:
+    """Brute-force merge-path tile coordinates: int32 array [T+1, 2] of (row, nz)."""
+    off = _np(row_offsets, np.int32)
+    rows = off.size - 1
+    nnz = int(off[-1]) if rows > 0 else 0
+    T = (rows + nnz + L - 1) // L
+    out = np.empty((T + 1, 2), np.int32)
+    got = lib().oracle_partition(rows, nnz, _ptr(off), L, _ptr(out))
+    if got != T:
+        raise ValueError("bad partition arguments")
+    return out
+
+
+def shard_bounds(row_offsets, G: int) -> np.ndarray:
+    off = _np(row_offsets, np.int32)
+    out = np.empty(G + 1, np.int64)
+    lib().oracle_shard_bounds(off.size - 1, _ptr(off), G, _ptr(out))
+    return out
+
+
+def num_threads() -> int:
+    return int(lib().oracle_num_threads())

@@ -1,0 +1,149 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU reference for the hot path of
+ * arXiv 2212.08964 (CSR SpMV y = A x under a load-balancing schedule).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code,
+ * header, table or helper with paper_2212_08964_b200/ (the CUDA product path), and
+ * the product never calls it.
+ *
+ * Citations: "P:L" = /root/reference/PAPER.md line L (section / algorithm in brackets).
+ *
+ * Precision: every fp32 input is widened to double; a product of two fp32 values is
+ * exact in double (24+24 <= 53 significand bits), sums are taken in row order in double.
+ *
+ * Parity status: every function here is pinned by tests/test_oracle_pins.py
+ * (dense brute force, closed forms, invariants, independent derivations); nothing is
+ * "parity unpinned".
+ */
+#include <stdint.h>
+#include <stddef.h>
+#include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+/*
+ * SpMV by definition: y = A x for A in CSR (P:123 [Ch.3 intro]: "SpMV computes the output
+ * vector y = Ax"; P:149 [Sec. CSR]; Listing 3: for each row, sum += values[nz] *
+ * x[indices[nz]] over the row's nonzeros, then y[row] = sum).
+ * Also returns s[i] = sum_k |a_ik x_k| (the tolerance scale of BASELINE.json north_star).
+ * Empty rows give y = +0 (P:982 assigns the zero-initialised sum).
+ */
+void oracle_spmv(int64_t rows, const int32_t *row_offsets, const int32_t *col_idx,
+                 const float *values, const float *x, double *y, double *s)
+{
+    for (int64_t i = 0; i < rows; ++i) {
+        double acc = 0.0, mag = 0.0;
+        for (int64_t k = row_offsets[i]; k < row_offsets[i + 1]; ++k) {
+            double p = (double)values[k] * (double)x[col_idx[k]];
+            acc += p;
+            mag += fabs(p);
+        }
+        y[i] = acc;
+        if (s) s[i] = mag;
+    }
+}
+
+/* The same definition, rows split across OpenMP threads (used only to time the CPU
+ * baseline on the host's cores; the arithmetic per row is identical). */
+void oracle_spmv_omp(int64_t rows, const int32_t *row_offsets, const int32_t *col_idx,
+                     const float *values, const float *x, double *y, double *s)
+{
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t i = 0; i < rows; ++i) {
+        double acc = 0.0, mag = 0.0;
+        for (int64_t k = row_offsets[i]; k < row_offsets[i + 1]; ++k) {
+            double p = (double)values[k] * (double)x[col_idx[k]];
+            acc += p;
+            mag += fabs(p);
+        }
+        y[i] = acc;
+        if (s) s[i] = mag;
+    }
+}
+
+int oracle_num_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+/*
+ * SpMV on a set of selected rows whose nonzeros were gathered into a packed CSR
+ * (sel_offsets[n_sel+1] indexes sel_cols / sel_vals).  Used for sampled parity at
+ * full size, where the whole matrix is too big to evaluate on the host in the test.
+ */
+void oracle_spmv_packed(int64_t n_sel, const int64_t *sel_offsets, const int32_t *sel_cols,
+                        const float *sel_vals, const float *x, double *y, double *s)
+{
+    for (int64_t r = 0; r < n_sel; ++r) {
+        double acc = 0.0, mag = 0.0;
+        for (int64_t k = sel_offsets[r]; k < sel_offsets[r + 1]; ++k) {
+            double p = (double)sel_vals[k] * (double)x[sel_cols[k]];
+            acc += p;
+            mag += fabs(p);
+        }
+        y[r] = acc;
+        if (s) s[r] = mag;
+    }
+}
+
+/*
+ * Merge-path partition by brute force: walk the merge of list A = the row ends
+ * (row i ends after its off[i+1] nonzeros) and list B = the nonzero indices 0..nnz-1,
+ * one merge item per step, exactly as the merge-path schedule defines the work
+ * (P:292 [Sec. Work-Oriented]: "a work item as either a nonzero element or an output";
+ * "2-D split of the grid created using the row-offsets and the nonzero indices";
+ * P:1021 [Sec. Merge-path load balancing]: nnzs + rows work divided evenly).
+ * The coordinate (i, j) = (#row ends consumed, #nonzeros consumed) is recorded whenever the
+ * step count equals d_t = min(t * L, rows + nnz), t = 0..T, T = ceil((rows+nnz)/L)
+ * (Alg.3, with the ceil reading of items_per_thread -- DESIGN.md reading R2).
+ * Tie-break (R1): when off[i+1] == j the row end is taken first, because
+ * CSR rows are half-open and nonzero j belongs to a later row.
+ * coords receives (T+1) pairs (row, nz), row-major.  Returns T, or -1 on bad input.
+ */
+int64_t oracle_partition(int64_t rows, int64_t nnz, const int32_t *row_offsets, int64_t L,
+                         int32_t *coords)
+{
+    if (L <= 0 || rows < 0 || nnz < 0) return -1;
+    int64_t total = rows + nnz;
+    int64_t T = (total + L - 1) / L;
+    int64_t i = 0, j = 0, t = 0, step = 0;
+    for (;;) {
+        int64_t d_t = t * L < total ? t * L : total;
+        while (t <= T && step == d_t) {
+            coords[2 * t] = (int32_t)i;
+            coords[2 * t + 1] = (int32_t)j;
+            ++t;
+            d_t = t * L < total ? t * L : total;
+        }
+        if (t > T || step == total) break;
+        /* one merge item */
+        if (i < rows && (j == nnz || row_offsets[i + 1] <= j)) ++i;  /* row end i */
+        else ++j;                                                      /* nonzero j */
+        ++step;
+    }
+    return T;
+}
+
+/*
+ * Row-shard bounds for G ranks by equal nnz (reading R9; the paper has no
+ * multi-GPU design, P:784 / P:2187-2192): b_0 = 0, b_G = rows, and for 0 < g < G,
+ * b_g = min{ r : off[r] >= ceil(g * nnz / G) }, found by a linear scan.
+ */
+void oracle_shard_bounds(int64_t rows, const int32_t *row_offsets, int32_t G, int64_t *bounds)
+{
+    int64_t nnz = rows > 0 ? row_offsets[rows] : 0;
+    bounds[0] = 0;
+    int64_t r = 0;
+    for (int32_t g = 1; g < G; ++g) {
+        int64_t target = (g * nnz + G - 1) / G;
+        while (r < rows && row_offsets[r] < target) ++r;
+        bounds[g] = r;
+    }
+    bounds[G] = rows;
+}
