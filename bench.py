@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark of the SpMV hot path (arXiv 2212.08964) on B200 -- prints ONE JSON line.
+
+  python bench.py [--gpus N --steps K --warmup W] [--config c3] [--schedule merge_path]
+  python bench.py --impl reference ...      # the CPU oracle arm (rank 0 only)
+
+A "step" is one pass of the whole merge-path method over the workload: lb_partition (Alg.3
+2DSearch), the tile processor and the carry fix-up, all inside one lb_spmv_ex(REPARTITION) call
+(N=1).  With N>1 (torchrun, one process per GPU) a step is lb_spmv_multi: the rank's equal-nnz
+row shard of R-MAT scale-26 followed by the NCCL all-gather of y.
+
+value = nonzeros processed by all ranks / max-over-ranks step time, in GNZ/s.  Inputs are
+resident in HBM when the timed region starts; they are larger than L2 (no flush between steps).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+import torch
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import lbgen  # noqa: E402
+
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback (only if MEASURED_PEAKS.json is absent)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=500)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=None, help="c1..c6 (default: c3 at N=1, c5 at N>1)")
+    ap.add_argument("--schedule", default="merge_path")
+    ap.add_argument("--items-per-tile", type=int, default=2048)
+    ap.add_argument("--no-extras", action="store_true", help="skip e2e / cpu_baseline / clocks (profiling runs)")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0, help="budget for the cpu_baseline sample")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        if "hbm_gbs" in d:
+            return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (torch copy, read+write)"
+    return FALLBACK_HBM_GBS, "fallback 6.65 TB/s (B200_PROFILING.md; MEASURED_PEAKS.json absent)"
+
+
+def compulsory_bytes(rows, cols, nnz):
+    """col+val 8 B/nnz, offsets 4(rows+1), y 4 rows, x 4 cols (read at least once)."""
+    return 8 * nnz + 4 * (rows + 1) + 4 * rows + 4 * cols
+
+
+def ncu_traffic(cfg, sched, L):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    e = d.get(f"{cfg}/{sched}/L{L}")
+    return None if e is None else e.get("dram_bytes_per_launch")
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms while running."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,utilization.gpu,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.p = None
+        self.out = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p is not None:
+            self.p.terminate()
+            try:
+                self.out, _ = self.p.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.p.kill()
+                self.out, _ = self.p.communicate()
+
+    def summary(self):
+        if not self.out:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        rows = []
+        for ln in self.out.strip().splitlines():
+            f = [c.strip() for c in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                rows.append(dict(sm=float(f[1]), smax=float(f[2]), util=float(f[4]),
+                                 hw=f[5], hwt=f[6], swt=f[7], pcap=f[8]))
+            except ValueError:
+                continue
+        load = [r for r in rows if r["util"] > 0] or rows
+        if not load:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        names = {"hw": "hw_slowdown", "hwt": "hw_thermal_slowdown", "swt": "sw_thermal_slowdown",
+                 "pcap": "sw_power_cap"}
+        reasons = sorted({n for r in load for k, n in names.items() if r[k].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(r["sm"] for r in load), "sm_max_mhz": max(r["smax"] for r in load),
+                "reasons": reasons, "samples": len(load)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ----------------------------------------------------------------------------- reference arm (CPU oracle)
+
+def cpu_sample(A: lbgen.Csr, x: torch.Tensor, target_nnz: int):
+    """Leading rows of the workload holding ~target_nnz nonzeros, as host arrays."""
+    off = A.row_offsets
+    r = int(torch.searchsorted(off.to(torch.int64), torch.tensor([target_nnz], device=off.device)).item())
+    r = max(1, min(r, A.rows))
+    o = off[: r + 1].cpu()
+    n = int(o[-1])
+    return o, A.col_idx[:n].cpu(), A.values[:n].cpu(), x.cpu(), r, n
+
+
+def time_oracle(sample, seconds: float, min_reps: int = 1):
+    import oracle
+    o, c, v, xx, r, n = sample
+    oracle.spmv(o, c, v, xx, threads=True)  # warm
+    reps, t0 = 0, time.perf_counter()
+    while reps < min_reps or time.perf_counter() - t0 < seconds:
+        oracle.spmv(o, c, v, xx, threads=True)
+        reps += 1
+    dt = time.perf_counter() - t0
+    return n * reps / dt / 1e9, reps, dt
+
+
+def run_reference(args, cfg):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    A = lbgen.make_config(cfg, "float", device=dev)
+    x = lbgen.x_for_config(cfg, A.cols, "float", device=dev)
+    sample = cpu_sample(A, x, 16_000_000 if cfg != "c1" else A.nnz)
+    o, c, v, xx, r, n = sample
+    for _ in range(args.warmup):
+        oracle.spmv(o, c, v, xx, threads=True)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.spmv(o, c, v, xx, threads=True)
+    dt = time.perf_counter() - t0
+    val = n * args.steps / dt / 1e9
+    desc = f"leading {r} rows ({n} nnz) of {cfg}, full x; oracle.spmv_omp (fp64) per step"
+    print(json.dumps({
+        "impl": "reference", "metric": "SpMV GNZ/s", "value": round(val, 4), "unit": "GNZ/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg, "desc": lbgen.CONFIG_DESC.get(cfg, cfg), "sample": desc},
+        "cpu_baseline": {"value": round(val, 4), "unit": "GNZ/s", "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": desc},
+        "e2e": {"value": round(val, 4), "unit": "GNZ/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_single(args, cfg):
+    import paper_2212_08964_b200 as lb
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    A = lbgen.make_config(cfg, "float", device=dev)
+    x = lbgen.x_for_config(cfg, A.cols, "float", device=dev)
+    rows, cols, nnz = A.rows, A.cols, A.nnz
+    M = lb.CsrMatrix.from_csr(A, device=dev, validate=True)
+    M.set_items_per_tile(args.items_per_tile)
+    y = torch.empty(rows, device=dev)
+    stream = torch.cuda.current_stream()
+    sched = args.schedule
+
+    def step():
+        M.spmv(x, y, sched, repartition=True)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    sampler = ClockSampler(torch.cuda.current_device()) if not args.no_extras else None
+    if sampler:
+        sampler.__enter__()
+        # soak so the sampler sees steady-state clocks even if K steps are short
+        t0 = time.perf_counter()
+        while time.perf_counter() - t0 < 1.0:
+            step()
+        torch.cuda.synchronize()
+    n0 = lb.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = lb.launch_count() - n0
+    if sampler:
+        sampler.__exit__()
+    ms = e0.elapsed_time(e1) / args.steps
+    value = nnz / (ms * 1e-3) / 1e9
+
+    # dominant kernel: per-phase CUDA events on the launching stream
+    phases = []
+    for _ in range(20):
+        phases.append(M.phase_times(x, y, sched))
+    ph = np.mean(np.array(phases), axis=0)
+    main_ms = float(ph[1])
+    alg = compulsory_bytes(rows, cols, nnz)
+    peak, peak_src = peak_hbm()
+    achieved = alg / (main_ms * 1e-3) / 1e9
+    rec = {
+        "metric": "SpMV GNZ/s", "value": round(value, 3), "unit": "GNZ/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (lbgen counter-hash generator, seeded)",
+        "config": {"workload": cfg, "desc": lbgen.CONFIG_DESC.get(cfg, cfg), "rows": rows, "cols": cols, "nnz": nnz,
+                   "schedule": sched, "items_per_tile": args.items_per_tile, "parallelism": "1 GPU",
+                   "values": "uniform [-1,1) fp32", "step": "lb_spmv_ex(REPARTITION): partition + tiles + fixup",
+                   "l2": "inputs (%.2f GB) larger than the 126 MB L2; no flush between steps" % (alg / 1e9)},
+        "gpu_launches": int(launches),
+        "phase_ms": {"partition": round(float(ph[0]), 5), "main": round(main_ms, 5), "fixup": round(float(ph[2]), 5)},
+        "roofline": {"bound": "hbm", "kernel": "merge_tile_kernel" if sched == "merge_path" else sched,
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": ncu_traffic(cfg, sched, args.items_per_tile), "algorithmic_bytes": alg,
+                     "peak_source": peak_src,
+                     "kernel_ms_from": "mean of 20 lb_spmv_phase_times calls (CUDA events on the launch stream)"},
+    }
+    if args.no_extras:
+        print(json.dumps(rec))
+        return
+    rec["clocks"] = sampler.summary()
+
+    # end to end through the public C-ABI call with host buffers (H2D + compute + D2H per step)
+    h = lb.HostSpmv(rows, cols, nnz, device=dev)
+    ho, hc, hv = A.row_offsets.cpu().pin_memory(), A.col_idx.cpu().pin_memory(), A.values.cpu().pin_memory()
+    hx, hy = x.cpu().pin_memory(), torch.empty(rows).pin_memory()
+    h(ho, hc, hv, hx, hy, sched)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        h(ho, hc, hv, hx, hy, sched)
+    dt = (time.perf_counter() - t0) / args.e2e_steps
+    rec["e2e"] = {"value": round(nnz / dt / 1e9, 3), "unit": "GNZ/s", "h2d_bytes_per_step": 4 * (rows + 1) + 8 * nnz + 4 * cols,
+                  "d2h_bytes_per_step": 4 * rows, "api": "lb_spmv_host (pinned host buffers)", "steps": args.e2e_steps}
+    del h
+    torch.cuda.empty_cache()
+
+    # CPU oracle on a bounded sample of the same workload
+    import oracle
+    sample = cpu_sample(A, x, 32_000_000 if cfg != "c1" else A.nnz)
+    gnz, reps, dt = time_oracle(sample, args.cpu_seconds)
+    rec["cpu_baseline"] = {"value": round(gnz, 4), "unit": "GNZ/s", "cores": oracle.num_threads(), "kind": "oracle",
+                           "sample": f"leading {sample[4]} rows ({sample[5]} nnz) of {cfg} with full x, {reps} reps "
+                                     f"in {dt:.1f} s (oracle.spmv_omp, fp64)"}
+    print(json.dumps(rec))
+
+
+def run_multi(args, cfg):
+    import torch.distributed as dist
+    import paper_2212_08964_b200 as lb
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    A = lbgen.make_config(cfg, "float", device=dev)
+    x = lbgen.x_for_config(cfg, A.cols, "float", device=dev)
+    rows, cols, nnz = A.rows, A.cols, A.nnz
+    b = lb.shard_bounds(A.row_offsets, world)
+    off, col, val = lb.shard_csr(A.row_offsets, A.col_idx, A.values, b, rank)
+    del A
+    torch.cuda.empty_cache()
+    M = lb.CsrMatrix(int(b[rank + 1] - b[rank]), cols, off, col, val, validate=True)
+    M.set_items_per_tile(args.items_per_tile)
+    comm = lb.Comm.from_process_group(local)
+    y = torch.empty(rows, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        comm.spmv_multi(M, b, x, y, args.schedule)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local) if (rank == 0 and not args.no_extras) else None
+    if sampler:
+        sampler.__enter__()
+    n0 = lb.launch_count()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = lb.launch_count() - n0
+    if sampler:
+        sampler.__exit__()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    # SpMV-only (no exchange) time of this rank's shard
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    f0.record(stream)
+    for _ in range(args.steps):
+        M.spmv(x, y[int(b[rank]):int(b[rank + 1])], args.schedule)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    spmv_ms_local = f0.elapsed_time(f1) / args.steps
+    t = torch.tensor([ms_local, spmv_ms_local], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms, spmv_ms = float(t[0]), float(t[1])
+    if rank == 0:
+        rec = {
+            "metric": "SpMV GNZ/s", "value": round(nnz / (ms * 1e-3) / 1e9, 3), "unit": "GNZ/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (lbgen, seeded)",
+            "config": {"workload": cfg, "desc": lbgen.CONFIG_DESC.get(cfg, cfg), "rows": rows, "nnz": nnz,
+                       "schedule": args.schedule, "parallelism": f"row shards x{world} (equal nnz), NCCL all-gather of y",
+                       "step": "lb_spmv_multi: shard SpMV + all-gather(v) of y",
+                       "l2": "inputs larger than L2; no flush"},
+            "gpu_launches": int(launches),
+            "spmv_only": {"value": round(nnz / (spmv_ms * 1e-3) / 1e9, 3), "unit": "GNZ/s", "ms": round(spmv_ms, 5)},
+            "e2e": None,
+        }
+        if sampler:
+            rec["clocks"] = sampler.summary()
+        print(json.dumps(rec))
+    comm.close()
+    dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    world, rank, _ = dist_env()
+    if args.impl == "reference":
+        cfg = args.config or ("c3" if world == 1 else "c5")
+        run_reference(args, cfg)
+        return
+    if world > 1:
+        run_multi(args, args.config or "c5")
+    else:
+        run_single(args, args.config or "c3")
+
+
+if __name__ == "__main__":
+    main()

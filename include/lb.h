@@ -1,0 +1,212 @@
+/*
+ * lb.h -- C ABI of liblb.so: CSR SpMV y = A x under a programmable load-balancing
+ * schedule, B200-native (sm_100a).  The hot path of arXiv 2212.08964 (Osama, "GPU load
+ * balancing"), Ch.3-4.
+ *
+ * Citations: "P:L" = PAPER.md line L [section / algorithm / listing].
+ *
+ * Conventions (all entry points)
+ *  - Plain pointers and sizes only.  "d_" pointers are CUDA device pointers, "h_" pointers
+ *    are host pointers.  A `stream` argument is a cudaStream_t passed as void* (NULL = the
+ *    legacy default stream).
+ *  - Ownership: every caller array is BORROWED.  A handle (lb_csr_t) keeps the device
+ *    pointers given to lb_csr_create; they must outlive the handle and stay unmodified while
+ *    calls are in flight.  A handle owns only its scratch (partition cache, carries), which is
+ *    allocated at create time so that lb_spmv can be captured in a CUDA graph.
+ *  - Asynchrony: every call is stream-ordered and does not synchronise the host, except
+ *    lb_csr_create(validate=1) (one sync to read the validation flag), lb_spmv_host (returns
+ *    with y on the host) and the lb_comm_* setup calls.
+ *  - Errors: a status code is returned; no exception crosses the ABI.  lb_last_error()
+ *    returns a thread-local message for the last failing call on this thread.
+ *  - Index widths: int32 row offsets and column indices, fp32 values, x and y (P:963-969,
+ *    Listing 3).  Sizes are int64; rows + nnz must be < 2^31 (reading R13).
+ *  - y is OVERWRITTEN (y = A x, not y += A x; "y[row] = sum", Alg.3).
+ *  - Empty rows produce y = +0 (P:982 with the zero-initialised sum); rows == 0 is a no-op.
+ *  - There is no CPU fallback: every compute call runs CUDA kernels of this library and
+ *    fails with LB_ERR_CUDA if no device is usable.
+ */
+#ifndef LB_H
+#define LB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  LB_OK = 0,
+  LB_ERR_INVALID_ARG = 1,  /* null pointer with non-zero size, negative size, rows+nnz >= 2^31,
+                              unknown schedule, unsupported items_per_tile, x aliasing y, ... */
+  LB_ERR_INVALID_CSR = 2,  /* validation failed: off[0] != 0, off not non-decreasing,
+                              off[rows] != nnz, or a column index outside [0, cols) */
+  LB_ERR_UNSUPPORTED = 3,  /* feature not available in this build (e.g. NCCL not loadable) */
+  LB_ERR_OOM = 4,          /* device or host allocation failed */
+  LB_ERR_CUDA = 5,         /* a CUDA runtime call failed (message in lb_last_error) */
+  LB_ERR_NCCL = 6          /* an NCCL call failed or reported an asynchronous error */
+} lb_status_t;
+
+/*
+ * Load-balancing schedules ("update a single C++ enum ... to select the desired load
+ * balancing schedule").
+ *  THREAD_MAPPED   one row (work tile) per thread, atoms of the row processed sequentially,
+ *                  grid-stride over rows; 256 threads per block, ceil(rows/256) blocks
+ *                  (P:211-237 [Sec. Thread-Mapped]; Listings 2-3 P:904-990).
+ *  GROUP_MAPPED    group of G = 32 lanes (a warp) takes G consecutive rows per round: lanes
+ *                  load their row's atom count, the group prefix-sums them, lanes stride the
+ *                  group's atom pool by G and find each atom's row by binary search in the
+ *                  prefix sum (P:241-281 [Sec. Group-Mapped], Alg.2).  Products
+ *                  are summed per row by a deterministic segmented reduction (reading R8).
+ *  MERGE_PATH      work-oriented merge-path: rows + nnz merge items split evenly into tiles of
+ *                  L items; per tile the (row, nz) start comes from the 2-D diagonal search;
+ *                  complete rows are written, the trailing partial row is carried out and
+ *                  fixed up after all tiles (P:283-339 [Sec. Work-Oriented], Alg.3;
+ *                  P:1018-1028 [Sec. Merge-path load balancing]).
+ *  BLOCK_MAPPED    GROUP_MAPPED with G = 256 (a CTA) -- the block-mapped instance the paper gets
+ *                  "for free" from the group-mapped schedule (table).
+ */
+typedef enum {
+  LB_SCHED_THREAD_MAPPED = 0,
+  LB_SCHED_GROUP_MAPPED = 1,
+  LB_SCHED_MERGE_PATH = 2,
+  LB_SCHED_BLOCK_MAPPED = 3
+} lb_schedule_t;
+
+typedef struct lb_csr_s* lb_csr_t;   /* opaque CSR handle (borrowed arrays + owned scratch) */
+typedef struct lb_comm_s* lb_comm_t; /* opaque multi-GPU communicator (wraps an ncclComm_t) */
+
+/* Default merge-path tile length L (merge items per tile) used by lb_spmv. */
+#define LB_DEFAULT_ITEMS_PER_TILE 2048
+
+/*
+ * lb_csr_create -- borrow a CSR matrix (P:149 [Sec. CSR]: row offsets = prefix sum of row
+ * lengths, column indices and values in row-major order).
+ *  rows, cols, nnz     matrix shape and number of stored entries (>= 0; rows + nnz < 2^31).
+ *  d_row_offsets       int32[rows+1], d_col_idx int32[nnz], d_values fp32[nnz] (device).
+ *  validate            1: run the validation kernel (off[0] = 0, off non-decreasing,
+ *                      off[rows] = nnz, 0 <= col < cols) and synchronise `stream` once to read
+ *                      the result; failure returns LB_ERR_INVALID_CSR naming the first
+ *                      offending index.  0: trust the caller (no sync).
+ *  out                 receives the handle; release with lb_csr_destroy.
+ * Duplicate and unsorted column indices are allowed (SpMV is linear in stored entries).
+ */
+lb_status_t lb_csr_create(int64_t rows, int64_t cols, int64_t nnz, const int32_t* d_row_offsets,
+                          const int32_t* d_col_idx, const float* d_values, int32_t validate,
+                          void* stream, lb_csr_t* out);
+
+/* lb_csr_destroy -- free the handle's scratch (after all work using it has completed). */
+lb_status_t lb_csr_destroy(lb_csr_t A);
+
+/*
+ * lb_csr_set_items_per_tile -- choose the merge-path tile length L used by lb_spmv
+ * (0 = LB_DEFAULT_ITEMS_PER_TILE).  Supported: 1024, 2048, 4096 (256 threads x 4/8/16 items).
+ * Invalidates the cached partition.  Not thread-safe with respect to in-flight lb_spmv.
+ */
+lb_status_t lb_csr_set_items_per_tile(lb_csr_t A, int32_t items_per_tile);
+
+/*
+ * lb_partition_size -- number of merge-path tiles T = ceil((rows + nnz) / L) for tile length
+ * L = items_per_tile (0 = the handle's current L).  Host-only, no device work.
+ */
+lb_status_t lb_partition_size(lb_csr_t A, int32_t items_per_tile, int64_t* num_tiles);
+
+/*
+ * lb_partition -- merge-path partition (Alg.3 P:306-311 "2DSearch").
+ * For t = 0..T with d_t = min(t*L, rows+nnz), writes the coordinate
+ *   (i_t, j_t):  i_t = #{ k < rows : k + off[k+1] < d_t },  j_t = d_t - i_t
+ * (the number of row ends and of nonzeros that precede diagonal d_t in the merge of the row
+ * ends with the nonzero indices; a row end precedes nonzero off[k+1] -- reading R1).
+ *  items_per_tile  L >= 1 (any value; 0 = the handle's current L).
+ *  d_coords        int32[(T+1)*2] device buffer, (row, nz) pairs, caller-owned.
+ * Bit-exact: integer arithmetic only.
+ */
+lb_status_t lb_partition(lb_csr_t A, int32_t items_per_tile, int32_t* d_coords, void* stream);
+
+/*
+ * lb_spmv -- y = A x under schedule `sched` (Listing 3; Alg.3).
+ *  d_x  fp32[cols] device; d_y  fp32[rows] device (overwritten); x and y must not alias.
+ * MERGE_PATH uses the handle's cached partition at its L, computing it on the first call.
+ * Arithmetic: fp32 products and fp32 accumulation (reading R12); deterministic (bitwise
+ * identical results for identical inputs and launch configuration).
+ */
+lb_status_t lb_spmv(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_y, void* stream);
+
+/* Flags for lb_spmv_ex. */
+#define LB_SPMV_REPARTITION 1u /* MERGE_PATH: recompute the partition inside this call */
+
+/* lb_spmv_ex -- lb_spmv with flags (LB_SPMV_REPARTITION: the whole merge-path method --
+ * partition, tile processing, fix-up -- runs in this call; used by bench.py's step). */
+lb_status_t lb_spmv_ex(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_y, uint32_t flags,
+                       void* stream);
+
+/*
+ * lb_spmv_host -- end-to-end y = A x from HOST buffers (ideally pinned): copies the CSR arrays
+ * and x host->device into `d_workspace`, builds a transient handle (no validation), partitions,
+ * runs `sched`, copies y device->host and synchronises `stream` before returning.
+ *  d_workspace      device buffer of at least lb_spmv_host_workspace_size(rows, cols, nnz)
+ *                   bytes (caller-owned; reused across calls to avoid allocation).
+ */
+size_t lb_spmv_host_workspace_size(int64_t rows, int64_t cols, int64_t nnz);
+lb_status_t lb_spmv_host(int64_t rows, int64_t cols, int64_t nnz, const int32_t* h_row_offsets,
+                         const int32_t* h_col_idx, const float* h_values, const float* h_x, float* h_y,
+                         lb_schedule_t sched, void* d_workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * lb_spmv_phase_times -- diagnostics: run `sched` once with CUDA events between its kernels on
+ * `stream`, synchronise, and report milliseconds per phase in ms_out[3] = {partition, main
+ * kernel, fix-up} (unused phases are 0).  MERGE_PATH recomputes the partition.
+ */
+lb_status_t lb_spmv_phase_times(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_y, void* stream,
+                                float* ms_out);
+
+/*
+ * lb_shard_bounds -- host-only: row-shard bounds for `nranks` GPUs with equal nonzeros
+ * (reading R9; the paper defers multi-GPU to future work):
+ *   b_0 = 0, b_G = rows, b_g = min{ r : off[r] >= ceil(g * nnz / G) }   (0 < g < G).
+ *  h_row_offsets  int32[rows+1] host;  h_bounds  int64[nranks+1] host (output).
+ */
+lb_status_t lb_shard_bounds(const int32_t* h_row_offsets, int64_t rows, int32_t nranks, int64_t* h_bounds);
+
+/*
+ * Multi-GPU (one process per GPU).  NCCL is loaded at run time (dlopen of libnccl.so.2, the
+ * copy already mapped by PyTorch if any); LB_ERR_UNSUPPORTED if it cannot be loaded.
+ *  lb_comm_unique_id  rank 0 creates the 128-byte NCCL unique id (ship it to the other ranks
+ *                     with any host transport, e.g. torch.distributed.broadcast_object_list).
+ *  lb_comm_init       every rank: join communicator `id` as `rank` of `nranks` on CUDA `device`.
+ */
+lb_status_t lb_comm_unique_id(uint8_t id_out[128]);
+lb_status_t lb_comm_init(const uint8_t id[128], int32_t rank, int32_t nranks, int32_t device, lb_comm_t* out);
+lb_status_t lb_comm_destroy(lb_comm_t c);
+
+/*
+ * lb_spmv_multi -- one iteration of row-sharded SpMV: this rank computes
+ *   y_full[b_r .. b_{r+1}) = A_local x_full
+ * with `sched`, then all-gathers the shards so every rank holds the whole y_full
+ * (NCCL over NVLink, on `stream`, after the compute).
+ *  A_local   handle of this rank's row shard (rows b_{r+1}-b_r, GLOBAL column ids, offsets
+ *            rebased to start at 0).
+ *  h_bounds  int64[nranks+1] host, identical on every rank (from lb_shard_bounds).
+ *  d_x_full  fp32[cols] (replicated); d_y_full fp32[b_G] (must not alias d_x_full).
+ */
+lb_status_t lb_spmv_multi(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, const int64_t* h_bounds,
+                          const float* d_x_full, float* d_y_full, void* stream);
+
+/* lb_allgather_rows -- the exchange step of lb_spmv_multi alone: rank r contributes
+ * d_y_full[b_r .. b_{r+1}) and receives every other rank's slice in place. */
+lb_status_t lb_allgather_rows(lb_comm_t c, const int64_t* h_bounds, float* d_y_full, void* stream);
+
+/* Last error message of the calling thread ("" if none). */
+const char* lb_last_error(void);
+
+/* Number of CUDA kernels this library has launched in this process (for bench accounting). */
+uint64_t lb_launch_count(void);
+
+/* Library version string. */
+const char* lb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LB_H */

@@ -1,0 +1,549 @@
+// lb_api.cu -- C ABI of liblb.so (declared and documented in include/lb.h).
+// Handle management, argument checking, launch configuration and the multi-GPU layer.
+// All compute runs in the kernels of lb_kernels.cuh; there is no CPU fallback.
+#include "lb.h"
+#include "lb_kernels.cuh"
+
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <atomic>
+#include <climits>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+lb_status_t fail(lb_status_t st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define LB_CUDA(call)                                                                         \
+  do {                                                                                        \
+    cudaError_t e_ = (call);                                                                  \
+    if (e_ != cudaSuccess) return fail(LB_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); \
+  } while (0)
+
+#define LB_LAUNCHED()                                                                                      \
+  do {                                                                                                     \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                                   \
+    if (e_ != cudaSuccess) return fail(LB_ERR_CUDA, "kernel launch (%s:%d): %s", __FILE__, __LINE__,        \
+                                       cudaGetErrorString(e_));                                            \
+  } while (0)
+
+constexpr int kNT = 256;
+constexpr int kMaxCtas = 8192;      // carry slots per handle (>= SMs x resident CTAs)
+constexpr int kMinTile = 1024;      // smallest supported L: sizes the partition cache
+
+struct DeviceInfo {
+  int sm_count = 0;
+  int grid_1024 = 0, grid_2048 = 0;  // persistent grid of the merge-path kernel per L
+};
+
+DeviceInfo g_dev[64];
+std::mutex g_dev_mu;
+
+using stream_t = cudaStream_t;
+inline stream_t S(void* s) { return reinterpret_cast<stream_t>(s); }
+
+template <int L, bool VEC>
+size_t merge_smem() { return sizeof(typename lbk::MergeCfg<kNT, L, VEC>::Smem); }
+
+template <int L, bool VEC>
+lb_status_t merge_prepare(int* blocks_per_sm) {
+  auto k = lbk::merge_tile_kernel<kNT, L, VEC>;
+  LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)merge_smem<L, VEC>()));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k, kNT, merge_smem<L, VEC>()));
+  return LB_OK;
+}
+
+lb_status_t device_info(int dev, const DeviceInfo** out) {
+  if (dev < 0 || dev >= 64) return fail(LB_ERR_INVALID_ARG, "device ordinal %d out of range", dev);
+  std::lock_guard<std::mutex> g(g_dev_mu);
+  DeviceInfo& d = g_dev[dev];
+  if (d.sm_count == 0) {
+    LB_CUDA(cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, dev));
+    int b1 = 0, b2 = 0, b3 = 0, b4 = 0;
+    lb_status_t st;
+    if ((st = merge_prepare<1024, true>(&b1)) != LB_OK) return st;
+    if ((st = merge_prepare<1024, false>(&b2)) != LB_OK) return st;
+    if ((st = merge_prepare<2048, true>(&b3)) != LB_OK) return st;
+    if ((st = merge_prepare<2048, false>(&b4)) != LB_OK) return st;
+    d.grid_1024 = d.sm_count * std::max(1, std::min(b1, b2));
+    d.grid_2048 = d.sm_count * std::max(1, std::min(b3, b4));
+  }
+  *out = &d;
+  return LB_OK;
+}
+
+}  // namespace
+
+struct lb_csr_s {
+  int64_t rows = 0, cols = 0, nnz = 0;
+  const int32_t* off = nullptr;
+  const int32_t* col = nullptr;
+  const float* val = nullptr;
+  int device = 0;
+  const DeviceInfo* dev = nullptr;
+  bool vec = true;            // col/val 16-byte aligned -> 128-bit loads
+  int L = LB_DEFAULT_ITEMS_PER_TILE;
+  bool coords_valid = false;
+  bool owns_scratch = true;
+  int2* coords = nullptr;     // partition cache [(T_max+1)]
+  int* carry_row = nullptr;   // [kMaxCtas]
+  float* carry_val = nullptr; // [kMaxCtas]
+  int* flags = nullptr;       // [4] validation flags
+};
+
+namespace {
+
+int64_t num_tiles(int64_t rows, int64_t nnz, int64_t L) { return (rows + nnz + L - 1) / L; }
+
+size_t align256(size_t n) { return (n + 255) & ~size_t(255); }
+
+size_t scratch_bytes(int64_t rows, int64_t nnz) {
+  return align256((num_tiles(rows, nnz, kMinTile) + 1) * sizeof(int2)) + align256(kMaxCtas * sizeof(int)) +
+         align256(kMaxCtas * sizeof(float)) + align256(4 * sizeof(int));
+}
+
+void carve_scratch(lb_csr_s* A, char* p) {
+  A->coords = reinterpret_cast<int2*>(p);
+  p += align256((num_tiles(A->rows, A->nnz, kMinTile) + 1) * sizeof(int2));
+  A->carry_row = reinterpret_cast<int*>(p);
+  p += align256(kMaxCtas * sizeof(int));
+  A->carry_val = reinterpret_cast<float*>(p);
+  p += align256(kMaxCtas * sizeof(float));
+  A->flags = reinterpret_cast<int*>(p);
+}
+
+lb_status_t check_shape(int64_t rows, int64_t cols, int64_t nnz) {
+  if (rows < 0 || cols < 0 || nnz < 0) return fail(LB_ERR_INVALID_ARG, "negative size (rows=%lld cols=%lld nnz=%lld)",
+                                                   (long long)rows, (long long)cols, (long long)nnz);
+  if (rows + nnz >= (int64_t)INT_MAX || cols >= (int64_t)INT_MAX)
+    return fail(LB_ERR_INVALID_ARG, "rows + nnz and cols must be < 2^31 (int32 indices)");
+  if (nnz > 0 && cols == 0) return fail(LB_ERR_INVALID_ARG, "nnz > 0 with cols == 0");
+  return LB_OK;
+}
+
+lb_status_t init_handle(lb_csr_s* A, int64_t rows, int64_t cols, int64_t nnz, const int32_t* off, const int32_t* col,
+                        const float* val) {
+  A->rows = rows; A->cols = cols; A->nnz = nnz;
+  A->off = off; A->col = col; A->val = val;
+  LB_CUDA(cudaGetDevice(&A->device));
+  lb_status_t st = device_info(A->device, &A->dev);
+  if (st != LB_OK) return st;
+  A->vec = (reinterpret_cast<uintptr_t>(col) % 16 == 0) && (reinterpret_cast<uintptr_t>(val) % 16 == 0);
+  return LB_OK;
+}
+
+lb_status_t run_validate(lb_csr_s* A, stream_t s) {
+  int init[4] = {0, INT_MAX, 0, INT_MAX};
+  LB_CUDA(cudaMemcpyAsync(A->flags, init, sizeof init, cudaMemcpyHostToDevice, s));
+  int64_t work = std::max<int64_t>(A->rows, A->nnz);
+  int grid = (int)std::min<int64_t>(std::max<int64_t>(1, (work + kNT - 1) / kNT), (int64_t)A->dev->sm_count * 16);
+  lbk::validate_kernel<<<grid, kNT, 0, s>>>((int)A->rows, (int)A->cols, (int)A->nnz, A->off, A->col, A->flags);
+  LB_LAUNCHED();
+  int got[4];
+  LB_CUDA(cudaMemcpyAsync(got, A->flags, sizeof got, cudaMemcpyDeviceToHost, s));
+  LB_CUDA(cudaStreamSynchronize(s));
+  if (got[0]) return fail(LB_ERR_INVALID_CSR, "row_offsets[0] != 0");
+  if (got[1] != INT_MAX) return fail(LB_ERR_INVALID_CSR, "row_offsets not monotone at row %d", got[1]);
+  if (got[2]) return fail(LB_ERR_INVALID_CSR, "row_offsets[rows] != nnz (%lld)", (long long)A->nnz);
+  if (got[3] != INT_MAX) return fail(LB_ERR_INVALID_CSR, "col_idx[%d] outside [0, %lld)", got[3], (long long)A->cols);
+  return LB_OK;
+}
+
+lb_status_t launch_partition(const lb_csr_s* A, int64_t L, int2* coords, stream_t s) {
+  const int64_t T = num_tiles(A->rows, A->nnz, L);
+  const int64_t n = T + 1;
+  const int grid = (int)((n + kNT - 1) / kNT);
+  lbk::partition_kernel<<<grid, kNT, 0, s>>>((int)A->rows, (int)A->nnz, A->off, L, T, coords);
+  LB_LAUNCHED();
+  return LB_OK;
+}
+
+template <int L, bool VEC>
+lb_status_t launch_merge_tiles(lb_csr_s* A, const float* x, float* y, int grid_max, int* grid_used, stream_t s) {
+  const int T = (int)num_tiles(A->rows, A->nnz, L);
+  int grid = std::min(T, std::min(grid_max, kMaxCtas));
+  const int tpc = (T + grid - 1) / grid;
+  grid = (T + tpc - 1) / tpc;  // every CTA owns >= 1 tile
+  lbk::MergeArgs a;
+  a.off = A->off; a.col = A->col; a.val = A->val; a.x = x; a.y = y;
+  a.coords = A->coords; a.rows = (int)A->rows; a.nnz = (int)A->nnz;
+  a.num_tiles = T; a.tiles_per_cta = tpc;
+  a.carry_row = A->carry_row; a.carry_val = A->carry_val;
+  lbk::merge_tile_kernel<kNT, L, VEC><<<grid, kNT, merge_smem<L, VEC>(), s>>>(a);
+  LB_LAUNCHED();
+  *grid_used = grid;
+  return LB_OK;
+}
+
+// Phase hooks for lb_spmv_phase_times (events recorded between phases when non-null).
+struct PhaseEvents {
+  cudaEvent_t ev[4];
+};
+
+lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y, uint32_t flags, stream_t s,
+                      PhaseEvents* pe) {
+  if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
+  if (A->rows == 0) return LB_OK;
+  if (!y || (!x && A->nnz > 0)) return fail(LB_ERR_INVALID_ARG, "null x or y");
+  if ((const void*)x == (const void*)y) return fail(LB_ERR_INVALID_ARG, "x and y must not alias");
+  if (pe) LB_CUDA(cudaEventRecord(pe->ev[0], s));
+  switch (sched) {
+    case LB_SCHED_THREAD_MAPPED: {
+      if (pe) LB_CUDA(cudaEventRecord(pe->ev[1], s));
+      // Listing 3: blocks of 256 threads, grid = ceil(rows / 256)
+      const int64_t grid = (A->rows + kNT - 1) / kNT;
+      lbk::thread_mapped_kernel<<<(unsigned)grid, kNT, 0, s>>>((int)A->rows, A->off, A->col, A->val, x, y);
+      LB_LAUNCHED();
+      if (pe) { LB_CUDA(cudaEventRecord(pe->ev[2], s)); LB_CUDA(cudaEventRecord(pe->ev[3], s)); }
+      return LB_OK;
+    }
+    case LB_SCHED_GROUP_MAPPED:
+    case LB_SCHED_BLOCK_MAPPED: {
+      if (pe) LB_CUDA(cudaEventRecord(pe->ev[1], s));
+      const int G = sched == LB_SCHED_GROUP_MAPPED ? 32 : 256;
+      const int64_t groups = (A->rows + G - 1) / G;
+      const int64_t groups_per_cta = kNT / G;
+      const int64_t grid = std::max<int64_t>(1, (groups + groups_per_cta - 1) / groups_per_cta);
+      if (G == 32)
+        lbk::group_mapped_kernel<32><<<(unsigned)grid, kNT, 0, s>>>((int)A->rows, A->off, A->col, A->val, x, y);
+      else
+        lbk::group_mapped_kernel<256><<<(unsigned)grid, kNT, 0, s>>>((int)A->rows, A->off, A->col, A->val, x, y);
+      LB_LAUNCHED();
+      if (pe) { LB_CUDA(cudaEventRecord(pe->ev[2], s)); LB_CUDA(cudaEventRecord(pe->ev[3], s)); }
+      return LB_OK;
+    }
+    case LB_SCHED_MERGE_PATH: {
+      lb_status_t st;
+      if (!A->coords_valid || (flags & LB_SPMV_REPARTITION)) {
+        if ((st = launch_partition(A, A->L, A->coords, s)) != LB_OK) return st;
+        A->coords_valid = true;
+      }
+      if (pe) LB_CUDA(cudaEventRecord(pe->ev[1], s));
+      int grid = 0;
+      if (A->L == 1024)
+        st = A->vec ? launch_merge_tiles<1024, true>(A, x, y, A->dev->grid_1024, &grid, s)
+                    : launch_merge_tiles<1024, false>(A, x, y, A->dev->grid_1024, &grid, s);
+      else
+        st = A->vec ? launch_merge_tiles<2048, true>(A, x, y, A->dev->grid_2048, &grid, s)
+                    : launch_merge_tiles<2048, false>(A, x, y, A->dev->grid_2048, &grid, s);
+      if (st != LB_OK) return st;
+      if (pe) LB_CUDA(cudaEventRecord(pe->ev[2], s));
+      lbk::fixup_kernel<<<(grid + kNT - 1) / kNT, kNT, 0, s>>>((int)A->rows, grid, A->carry_row, A->carry_val, y);
+      LB_LAUNCHED();
+      if (pe) LB_CUDA(cudaEventRecord(pe->ev[3], s));
+      return LB_OK;
+    }
+    default:
+      return fail(LB_ERR_INVALID_ARG, "unknown schedule id %d", (int)sched);
+  }
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+const char* lb_last_error(void) { return g_err.c_str(); }
+uint64_t lb_launch_count(void) { return g_launches.load(); }
+const char* lb_version(void) { return "liblb 0.1 (sm_100a)"; }
+
+lb_status_t lb_csr_create(int64_t rows, int64_t cols, int64_t nnz, const int32_t* d_row_offsets,
+                          const int32_t* d_col_idx, const float* d_values, int32_t validate, void* stream,
+                          lb_csr_t* out) {
+  g_err.clear();
+  if (!out) return fail(LB_ERR_INVALID_ARG, "null output handle pointer");
+  *out = nullptr;
+  lb_status_t st = check_shape(rows, cols, nnz);
+  if (st != LB_OK) return st;
+  if (!d_row_offsets) return fail(LB_ERR_INVALID_ARG, "null row_offsets");
+  if (nnz > 0 && (!d_col_idx || !d_values)) return fail(LB_ERR_INVALID_ARG, "null col_idx or values with nnz > 0");
+  lb_csr_s* A = new (std::nothrow) lb_csr_s();
+  if (!A) return fail(LB_ERR_OOM, "host allocation failed");
+  st = init_handle(A, rows, cols, nnz, d_row_offsets, d_col_idx, d_values);
+  if (st != LB_OK) { delete A; return st; }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, scratch_bytes(rows, nnz));
+  if (e != cudaSuccess) { delete A; return fail(LB_ERR_OOM, "cudaMalloc scratch: %s", cudaGetErrorString(e)); }
+  carve_scratch(A, static_cast<char*>(p));
+  if (validate) {
+    st = run_validate(A, S(stream));
+    if (st != LB_OK) { cudaFree(p); delete A; return st; }
+  }
+  *out = A;
+  return LB_OK;
+}
+
+lb_status_t lb_csr_destroy(lb_csr_t A) {
+  if (!A) return LB_OK;
+  if (A->owns_scratch && A->coords) cudaFree(A->coords);
+  delete A;
+  return LB_OK;
+}
+
+lb_status_t lb_csr_set_items_per_tile(lb_csr_t A, int32_t items_per_tile) {
+  if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
+  int L = items_per_tile == 0 ? LB_DEFAULT_ITEMS_PER_TILE : items_per_tile;
+  if (L != 1024 && L != 2048) return fail(LB_ERR_INVALID_ARG, "items_per_tile %d unsupported (1024, 2048)", L);
+  A->L = L;
+  A->coords_valid = false;
+  return LB_OK;
+}
+
+lb_status_t lb_partition_size(lb_csr_t A, int32_t items_per_tile, int64_t* n) {
+  if (!A || !n) return fail(LB_ERR_INVALID_ARG, "null argument");
+  int64_t L = items_per_tile == 0 ? A->L : items_per_tile;
+  if (L <= 0) return fail(LB_ERR_INVALID_ARG, "items_per_tile must be >= 1");
+  *n = num_tiles(A->rows, A->nnz, L);
+  return LB_OK;
+}
+
+lb_status_t lb_partition(lb_csr_t A, int32_t items_per_tile, int32_t* d_coords, void* stream) {
+  g_err.clear();
+  if (!A || !d_coords) return fail(LB_ERR_INVALID_ARG, "null argument");
+  int64_t L = items_per_tile == 0 ? A->L : items_per_tile;
+  if (L <= 0) return fail(LB_ERR_INVALID_ARG, "items_per_tile must be >= 1");
+  return launch_partition(A, L, reinterpret_cast<int2*>(d_coords), S(stream));
+}
+
+lb_status_t lb_spmv(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_y, void* stream) {
+  g_err.clear();
+  return spmv_impl(A, sched, d_x, d_y, 0u, S(stream), nullptr);
+}
+
+lb_status_t lb_spmv_ex(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_y, uint32_t flags, void* stream) {
+  g_err.clear();
+  return spmv_impl(A, sched, d_x, d_y, flags, S(stream), nullptr);
+}
+
+lb_status_t lb_spmv_phase_times(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_y, void* stream,
+                                float* ms_out) {
+  g_err.clear();
+  if (!ms_out) return fail(LB_ERR_INVALID_ARG, "null ms_out");
+  PhaseEvents pe;
+  for (auto& e : pe.ev) LB_CUDA(cudaEventCreate(&e));
+  lb_status_t st = spmv_impl(A, sched, d_x, d_y, LB_SPMV_REPARTITION, S(stream), &pe);
+  if (st == LB_OK && A->rows > 0) {
+    LB_CUDA(cudaEventSynchronize(pe.ev[3]));
+    for (int i = 0; i < 3; ++i) LB_CUDA(cudaEventElapsedTime(&ms_out[i], pe.ev[i], pe.ev[i + 1]));
+  } else if (st == LB_OK) {
+    ms_out[0] = ms_out[1] = ms_out[2] = 0.f;
+  }
+  for (auto& e : pe.ev) cudaEventDestroy(e);
+  return st;
+}
+
+size_t lb_spmv_host_workspace_size(int64_t rows, int64_t cols, int64_t nnz) {
+  if (rows < 0 || cols < 0 || nnz < 0) return 0;
+  return align256((rows + 1) * 4) + 2 * align256(nnz * 4) + align256(cols * 4) + align256(rows * 4) +
+         scratch_bytes(rows, nnz);
+}
+
+lb_status_t lb_spmv_host(int64_t rows, int64_t cols, int64_t nnz, const int32_t* h_row_offsets,
+                         const int32_t* h_col_idx, const float* h_values, const float* h_x, float* h_y,
+                         lb_schedule_t sched, void* d_workspace, size_t workspace_bytes, void* stream) {
+  g_err.clear();
+  lb_status_t st = check_shape(rows, cols, nnz);
+  if (st != LB_OK) return st;
+  if (!h_row_offsets || (rows > 0 && !h_y) || (nnz > 0 && (!h_col_idx || !h_values || !h_x)))
+    return fail(LB_ERR_INVALID_ARG, "null host buffer");
+  if (!d_workspace || workspace_bytes < lb_spmv_host_workspace_size(rows, cols, nnz))
+    return fail(LB_ERR_INVALID_ARG, "workspace too small (need %zu bytes)", lb_spmv_host_workspace_size(rows, cols, nnz));
+  stream_t s = S(stream);
+  char* p = static_cast<char*>(d_workspace);
+  int32_t* d_off = reinterpret_cast<int32_t*>(p); p += align256((rows + 1) * 4);
+  int32_t* d_col = reinterpret_cast<int32_t*>(p); p += align256(nnz * 4);
+  float* d_val = reinterpret_cast<float*>(p); p += align256(nnz * 4);
+  float* d_x = reinterpret_cast<float*>(p); p += align256(cols * 4);
+  float* d_y = reinterpret_cast<float*>(p); p += align256(rows * 4);
+  lb_csr_s A;
+  A.owns_scratch = false;
+  if ((st = init_handle(&A, rows, cols, nnz, d_off, d_col, d_val)) != LB_OK) return st;
+  carve_scratch(&A, p);
+  LB_CUDA(cudaMemcpyAsync(d_off, h_row_offsets, (rows + 1) * 4, cudaMemcpyHostToDevice, s));
+  if (nnz > 0) {
+    LB_CUDA(cudaMemcpyAsync(d_col, h_col_idx, nnz * 4, cudaMemcpyHostToDevice, s));
+    LB_CUDA(cudaMemcpyAsync(d_val, h_values, nnz * 4, cudaMemcpyHostToDevice, s));
+  }
+  if (cols > 0 && h_x) LB_CUDA(cudaMemcpyAsync(d_x, h_x, cols * 4, cudaMemcpyHostToDevice, s));
+  st = spmv_impl(&A, sched, d_x, d_y, LB_SPMV_REPARTITION, s, nullptr);
+  if (st != LB_OK) return st;
+  if (rows > 0) LB_CUDA(cudaMemcpyAsync(h_y, d_y, rows * 4, cudaMemcpyDeviceToHost, s));
+  LB_CUDA(cudaStreamSynchronize(s));
+  return LB_OK;
+}
+
+lb_status_t lb_shard_bounds(const int32_t* h_row_offsets, int64_t rows, int32_t nranks, int64_t* h_bounds) {
+  g_err.clear();
+  if (!h_row_offsets || !h_bounds) return fail(LB_ERR_INVALID_ARG, "null argument");
+  if (rows < 0 || nranks < 1) return fail(LB_ERR_INVALID_ARG, "rows < 0 or nranks < 1");
+  const int64_t nnz = h_row_offsets[rows];
+  h_bounds[0] = 0;
+  for (int32_t g = 1; g < nranks; ++g) {
+    const int64_t target = (g * nnz + nranks - 1) / nranks;  // ceil(g*nnz/G)
+    // lower bound: first r in [0, rows] with off[r] >= target
+    int64_t lo = 0, hi = rows;
+    while (lo < hi) {
+      int64_t mid = (lo + hi) >> 1;
+      if (h_row_offsets[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    h_bounds[g] = lo;
+  }
+  h_bounds[nranks] = rows;
+  return LB_OK;
+}
+
+}  // extern "C"
+
+// ============================================================================ multi-GPU (NCCL via dlopen)
+namespace {
+
+// Minimal NCCL ABI (stable since NCCL 2.0).
+typedef struct { char internal[128]; } nccl_uid_t;
+typedef void* nccl_comm_t;
+typedef int nccl_result_t;
+constexpr int kNcclFloat32 = 7;
+
+struct NcclApi {
+  bool loaded = false;
+  nccl_result_t (*GetUniqueId)(nccl_uid_t*) = nullptr;
+  nccl_result_t (*CommInitRank)(nccl_comm_t*, int, nccl_uid_t, int) = nullptr;
+  nccl_result_t (*CommDestroy)(nccl_comm_t) = nullptr;
+  nccl_result_t (*Broadcast)(const void*, void*, size_t, int, int, nccl_comm_t, cudaStream_t) = nullptr;
+  nccl_result_t (*GroupStart)() = nullptr;
+  nccl_result_t (*GroupEnd)() = nullptr;
+  nccl_result_t (*CommGetAsyncError)(nccl_comm_t, nccl_result_t*) = nullptr;
+  const char* (*GetErrorString)(nccl_result_t) = nullptr;
+};
+
+NcclApi g_nccl;
+std::mutex g_nccl_mu;
+
+lb_status_t nccl_load() {
+  std::lock_guard<std::mutex> g(g_nccl_mu);
+  if (g_nccl.loaded) return LB_OK;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD | RTLD_GLOBAL);  // PyTorch's copy, if mapped
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return fail(LB_ERR_UNSUPPORTED, "cannot load libnccl.so.2: %s", dlerror());
+#define SYM(name, field)                                                                       \
+  g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, name));                     \
+  if (!g_nccl.field) return fail(LB_ERR_UNSUPPORTED, "NCCL symbol %s missing", name);
+  SYM("ncclGetUniqueId", GetUniqueId)
+  SYM("ncclCommInitRank", CommInitRank)
+  SYM("ncclCommDestroy", CommDestroy)
+  SYM("ncclBroadcast", Broadcast)
+  SYM("ncclGroupStart", GroupStart)
+  SYM("ncclGroupEnd", GroupEnd)
+  SYM("ncclCommGetAsyncError", CommGetAsyncError)
+  SYM("ncclGetErrorString", GetErrorString)
+#undef SYM
+  g_nccl.loaded = true;
+  return LB_OK;
+}
+
+#define LB_NCCL(call)                                                                              \
+  do {                                                                                             \
+    nccl_result_t r_ = (call);                                                                     \
+    if (r_ != 0) return fail(LB_ERR_NCCL, "%s: %s", #call, g_nccl.GetErrorString(r_));             \
+  } while (0)
+
+}  // namespace
+
+struct lb_comm_s {
+  nccl_comm_t comm = nullptr;
+  int rank = 0, nranks = 1, device = 0;
+};
+
+extern "C" {
+
+lb_status_t lb_comm_unique_id(uint8_t id_out[128]) {
+  g_err.clear();
+  if (!id_out) return fail(LB_ERR_INVALID_ARG, "null id buffer");
+  lb_status_t st = nccl_load();
+  if (st != LB_OK) return st;
+  nccl_uid_t uid;
+  LB_NCCL(g_nccl.GetUniqueId(&uid));
+  memcpy(id_out, uid.internal, 128);
+  return LB_OK;
+}
+
+lb_status_t lb_comm_init(const uint8_t id[128], int32_t rank, int32_t nranks, int32_t device, lb_comm_t* out) {
+  g_err.clear();
+  if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) return fail(LB_ERR_INVALID_ARG, "bad comm arguments");
+  lb_status_t st = nccl_load();
+  if (st != LB_OK) return st;
+  LB_CUDA(cudaSetDevice(device));
+  nccl_uid_t uid;
+  memcpy(uid.internal, id, 128);
+  lb_comm_s* c = new (std::nothrow) lb_comm_s();
+  if (!c) return fail(LB_ERR_OOM, "host allocation failed");
+  nccl_result_t r = g_nccl.CommInitRank(&c->comm, nranks, uid, rank);
+  if (r != 0) { delete c; return fail(LB_ERR_NCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r)); }
+  c->rank = rank; c->nranks = nranks; c->device = device;
+  *out = c;
+  return LB_OK;
+}
+
+lb_status_t lb_comm_destroy(lb_comm_t c) {
+  if (!c) return LB_OK;
+  if (c->comm && g_nccl.loaded) g_nccl.CommDestroy(c->comm);
+  delete c;
+  return LB_OK;
+}
+
+lb_status_t lb_allgather_rows(lb_comm_t c, const int64_t* h_bounds, float* d_y_full, void* stream) {
+  g_err.clear();
+  if (!c || !h_bounds || !d_y_full) return fail(LB_ERR_INVALID_ARG, "null argument");
+  for (int k = 0; k < c->nranks; ++k)
+    if (h_bounds[k + 1] < h_bounds[k]) return fail(LB_ERR_INVALID_ARG, "bounds not monotone at %d", k);
+  if (c->nranks == 1) return LB_OK;
+  // all-gather(v) as one group of broadcasts, root k sends y[b_k, b_{k+1}) (SURVEY 8(e) option 1)
+  LB_NCCL(g_nccl.GroupStart());
+  for (int k = 0; k < c->nranks; ++k) {
+    const size_t n = (size_t)(h_bounds[k + 1] - h_bounds[k]);
+    if (n == 0) continue;
+    float* p = d_y_full + h_bounds[k];
+    nccl_result_t r = g_nccl.Broadcast(p, p, n, kNcclFloat32, k, c->comm, S(stream));
+    if (r != 0) { g_nccl.GroupEnd(); return fail(LB_ERR_NCCL, "ncclBroadcast: %s", g_nccl.GetErrorString(r)); }
+  }
+  LB_NCCL(g_nccl.GroupEnd());
+  nccl_result_t ar = 0;
+  LB_NCCL(g_nccl.CommGetAsyncError(c->comm, &ar));
+  if (ar != 0) return fail(LB_ERR_NCCL, "NCCL async error: %s", g_nccl.GetErrorString(ar));
+  return LB_OK;
+}
+
+lb_status_t lb_spmv_multi(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, const int64_t* h_bounds,
+                          const float* d_x_full, float* d_y_full, void* stream) {
+  g_err.clear();
+  if (!A_local || !c || !h_bounds || !d_x_full || !d_y_full) return fail(LB_ERR_INVALID_ARG, "null argument");
+  if ((const void*)d_x_full == (const void*)d_y_full) return fail(LB_ERR_INVALID_ARG, "x and y must not alias");
+  const int64_t b0 = h_bounds[c->rank], b1 = h_bounds[c->rank + 1];
+  if (b1 - b0 != A_local->rows)
+    return fail(LB_ERR_INVALID_ARG, "local shard has %lld rows, bounds say %lld", (long long)A_local->rows,
+                (long long)(b1 - b0));
+  lb_status_t st = spmv_impl(A_local, sched, d_x_full, d_y_full + b0, 0u, S(stream), nullptr);
+  if (st != LB_OK) return st;
+  return lb_allgather_rows(c, h_bounds, d_y_full, stream);
+}
+
+}  // extern "C"

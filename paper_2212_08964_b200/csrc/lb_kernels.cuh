@@ -1,0 +1,406 @@
+// lb_kernels.cuh -- sm_100a device code for CSR SpMV under three load-balancing schedules
+// (arXiv 2212.08964, Ch.3-4).  Citations "P:L" = PAPER.md line L.
+//
+// The path is bandwidth/gather bound (2 flops per >= 8 bytes); no tensor cores.
+// Design notes:
+//  * Merge-path tiles (L merge items each) are computed by lb_partition (Alg.3 2DSearch).
+//  * The tile processor is a persistent kernel: CTA c owns a contiguous run of tiles, so the
+//    partial row that crosses a tile boundary is carried in registers from tile to tile and
+//    only one carry per CTA reaches the fix-up ("first splitting the work across
+//    blocks, and then to threads within a block").
+//  * Inside a tile the nonzeros [j_t, j_{t+1}) are streamed with 128-bit loads aligned down to
+//    a 16-byte boundary (reverse-offset alignment) and summed per row with a
+//    warp-shuffle segmented scan; the rows [i_t, i_{t+1}) are written by a second, coalesced
+//    pass.  Both passes are strided across the CTA, so every thread does an even share of the
+//    tile's nonzeros and of its row ends.
+//  * x[col] gathers use plain LDG (L1-allocating): on B200 random 4-byte gathers are bound by
+//    ~1 L1tex line per clock per SM (~286 G/s measured, profiles/r01_microbench_gather.txt);
+//    TMA gather4 / bulk copies measured ~60 G/s, so they are not used for x.
+#pragma once
+#include <cstdint>
+#include <climits>
+#include <cuda_runtime.h>
+
+namespace lbk {
+
+constexpr unsigned kFull = 0xffffffffu;
+
+// ----------------------------------------------------------------------------- loads
+__device__ __forceinline__ int4 ld_cs_v4(const int* p) { return __ldcs(reinterpret_cast<const int4*>(p)); }
+__device__ __forceinline__ float4 ld_cs_v4(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ int ld_cs(const int* p) { return __ldcs(p); }
+__device__ __forceinline__ float ld_cs(const float* p) { return __ldcs(p); }
+__device__ __forceinline__ float ld_x(const float* p) { return __ldg(p); }
+
+// Segmented inclusive scan across a warp.  Pairs (f, v); combine(left, right) =
+// (left.f | right.f, right.f ? right.v : left.v + right.v).  With f = "a segment ended at or
+// after this element" it propagates the partial sum of the open segment; with f = "segment
+// head" it is a classic head-flag segmented scan.  Kogge-Stone: every result is a tree sum.
+__device__ __forceinline__ void warp_segscan_incl(bool& f, float& v, unsigned lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    float vo = __shfl_up_sync(kFull, v, o);
+    int fo = __shfl_up_sync(kFull, (int)f, o);
+    if (lane >= (unsigned)o) {
+      if (!f) v = vo + v;
+      f = f || fo;
+    }
+  }
+}
+
+__device__ __forceinline__ int warp_incl_scan_int(int v, unsigned lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(kFull, v, o);
+    if (lane >= (unsigned)o) v += t;
+  }
+  return v;
+}
+
+// ----------------------------------------------------------------------------- validation
+// flags[0]: off[0] != 0; flags[1]: first row r with off[r] > off[r+1] (INT_MAX if none);
+// flags[2]: off[rows] != nnz; flags[3]: first k with col[k] outside [0, cols) (INT_MAX if none).
+__global__ void validate_kernel(int rows, int cols, int nnz, const int* __restrict__ off,
+                                const int* __restrict__ col, int* flags) {
+  int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  if (tid == 0) {
+    flags[0] = off[0] != 0;
+    flags[2] = off[rows] != nnz;
+  }
+  for (int64_t r = tid; r < rows; r += stride)
+    if (off[r] > off[r + 1]) atomicMin(&flags[1], (int)r);
+  for (int64_t k = tid; k < nnz; k += stride) {
+    int c = col[k];
+    if (c < 0 || c >= cols) atomicMin(&flags[3], (int)k);
+  }
+}
+
+// ----------------------------------------------------------------------------- partition
+// Alg.3 P:306-311 (2DSearch) for every tile boundary t = 0..T:
+//   d = min(t*L, rows+nnz);  i = #{k < rows : k + off[k+1] < d};  j = d - i.
+// k + off[k+1] is the merge position of row end k (row end before nonzero off[k+1], reading
+// R1); it is strictly increasing in k, so i is a lower-bound binary search on
+// [max(0, d-nnz), min(d, rows)] (below d-nnz every row end precedes d).
+__global__ void partition_kernel(int rows, int nnz, const int* __restrict__ off, int64_t L, int64_t T,
+                                 int2* __restrict__ coords) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > T) return;
+  const int64_t total = (int64_t)rows + nnz;
+  const int64_t d = t * L < total ? t * L : total;
+  int lo = (int)(d - nnz > 0 ? d - nnz : 0);
+  int hi = (int)(d < rows ? d : rows);
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if ((int64_t)mid + __ldg(off + mid + 1) < d) lo = mid + 1;
+    else hi = mid;
+  }
+  coords[t] = make_int2(lo, (int)(d - lo));
+}
+
+// ----------------------------------------------------------------------------- merge-path tiles
+struct MergeArgs {
+  const int* off;
+  const int* col;
+  const float* val;
+  const float* x;
+  float* y;
+  const int2* coords;   // [T+1] tile coordinates (row, nz)
+  int rows, nnz;
+  int num_tiles;
+  int tiles_per_cta;
+  int* carry_row;       // [gridDim.x] row still open at the end of the CTA's run of tiles
+  float* carry_val;     // [gridDim.x] its partial sum over the CTA's tiles
+};
+
+template <int NT, int L, bool VEC>
+struct MergeCfg {
+  static constexpr int kSlots = (L + 6) / 4;                // 4-wide slots covering [j0&~3, j1)
+  static constexpr int kNV = (kSlots + NT - 1) / NT;        // slots per thread
+  static constexpr int kWarps = NT / 32;
+  static constexpr int kChunks = kNV * kWarps;              // 128-nonzero chunks per tile
+  static constexpr int kTailWords = (4 * kSlots + 31) / 32;
+  static_assert(kChunks <= 32, "chunk scan uses one warp");
+  static_assert(L % NT == 0, "tile length must be a multiple of the CTA width");
+  struct Smem {
+    unsigned tail[2][kTailWords];  // bit q set: local nonzero q (from j0&~3) ends its row
+    int rowend[2][L];              // local end (exclusive) of each row ending in the tile
+    float out[2][4 * kSlots];      // row sum at its last nonzero (tail positions only)
+    int cflag[kChunks];
+    float cval[kChunks];
+  };
+};
+
+// Persistent merge-path tile processor (Alg.3, per-tile reading R3-R5).
+template <int NT, int L, bool VEC>
+__global__ void __launch_bounds__(NT, 3) merge_tile_kernel(MergeArgs a) {
+  using Cfg = MergeCfg<NT, L, VEC>;
+  constexpr int NV = Cfg::kNV;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  typename Cfg::Smem& sm = *reinterpret_cast<typename Cfg::Smem*>(smem_raw);
+
+  const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t_begin = blockIdx.x * a.tiles_per_cta;
+  const int t_end = min(a.num_tiles, t_begin + a.tiles_per_cta);
+
+  for (int w = tid; w < 2 * Cfg::kTailWords; w += NT) (&sm.tail[0][0])[w] = 0u;
+  __syncthreads();
+
+  float cta_carry = 0.f;  // partial of the row open at the start of the current tile (this CTA's share)
+  int i_last = 0;
+  for (int t = t_begin; t < t_end; ++t) {
+    const int b = t & 1;
+    const int2 c0 = a.coords[t], c1 = a.coords[t + 1];
+    const int i0 = c0.x, j0 = c0.y, i1 = c1.x, j1 = c1.y;
+    const int nrows = i1 - i0;
+    const int jA = j0 & ~3;
+    const int nslots = (j1 - jA + 3) >> 2;
+    const int lo = j0 - jA, hi = j1 - jA;  // valid local positions [lo, hi)
+
+    // (1) stream this thread's column indices / values (evict-first)
+    int cidx[NV][4];
+    float vals[NV][4];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int s = v * NT + tid;
+      const int g = jA + 4 * s;
+      if (s < nslots) {
+        if (VEC && g + 4 <= a.nnz) {
+          int4 ci = ld_cs_v4(a.col + g);
+          float4 vi = ld_cs_v4(a.val + g);
+          cidx[v][0] = ci.x; cidx[v][1] = ci.y; cidx[v][2] = ci.z; cidx[v][3] = ci.w;
+          vals[v][0] = vi.x; vals[v][1] = vi.y; vals[v][2] = vi.z; vals[v][3] = vi.w;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const bool ok = g + e < a.nnz && 4 * s + e >= lo;
+            cidx[v][e] = ok ? ld_cs(a.col + g + e) : 0;
+            vals[v][e] = ok ? ld_cs(a.val + g + e) : 0.f;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) { cidx[v][e] = 0; vals[v][e] = 0.f; }
+      }
+    }
+    // (2) gather x for valid positions (all gathers issued before any use)
+    float xv[NV][4];
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int q0 = 4 * (v * NT + tid);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int q = q0 + e;
+        const bool ok = q >= lo && q < hi;
+        xv[v][e] = ok ? ld_x(a.x + cidx[v][e]) : 0.f;
+        if (!ok) vals[v][e] = 0.f;  // masked positions contribute exactly nothing
+      }
+    }
+    // (3) row ends of the tile -> tail bits + local ends (rows [i0, i1))
+    for (int r = tid; r < nrows; r += NT) {
+      const int e = __ldg(a.off + i0 + 1 + r) - jA;
+      const int s = r == 0 ? lo : __ldg(a.off + i0 + r) - jA;
+      sm.rowend[b][r] = e;
+      if (e > s) atomicOr(&sm.tail[b][(e - 1) >> 5], 1u << ((e - 1) & 31));
+    }
+    __syncthreads();
+
+    // (4) per-thread segmented sums over its 4-wide slots, then warp segmented scan
+    float tv[NV][4];       // value at each tail (before the carry-in of the first tail)
+    unsigned tails[NV];    // 4-bit tail mask per slot
+    bool lflag[NV];        // exclusive (lane) prefix flag
+    float lval[NV];        // exclusive (lane) prefix value
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const int q0 = 4 * (v * NT + tid);
+      const unsigned word = q0 < 4 * Cfg::kSlots ? sm.tail[b][q0 >> 5] : 0u;
+      const unsigned f4 = (word >> (q0 & 31)) & 0xFu;
+      tails[v] = f4;
+      float run = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        run = fmaf(vals[v][e], xv[v][e], run);
+        tv[v][e] = run;
+        if ((f4 >> e) & 1u) run = 0.f;
+      }
+      bool f = f4 != 0u;
+      float val = run;
+      warp_segscan_incl(f, val, lane);
+      // exclusive prefix for this lane
+      float ev = __shfl_up_sync(kFull, val, 1);
+      int ef = __shfl_up_sync(kFull, (int)f, 1);
+      lflag[v] = lane ? (bool)ef : false;
+      lval[v] = lane ? ev : 0.f;
+      if (lane == 31) {
+        sm.cflag[v * Cfg::kWarps + warp] = f;
+        sm.cval[v * Cfg::kWarps + warp] = val;
+      }
+    }
+    __syncthreads();
+
+    // (5) chunk-level scan (chunk c = v*warps + warp covers local nonzeros [128c, 128c+128))
+    bool cf = lane < (unsigned)Cfg::kChunks ? (bool)sm.cflag[lane] : false;
+    float cv = lane < (unsigned)Cfg::kChunks ? sm.cval[lane] : 0.f;
+    warp_segscan_incl(cf, cv, lane);
+    const float agg_val = __shfl_sync(kFull, cv, Cfg::kChunks - 1);
+    float ex_v = __shfl_up_sync(kFull, cv, 1);
+    int ex_f = __shfl_up_sync(kFull, (int)cf, 1);
+    if (lane == 0) { ex_v = 0.f; ex_f = 0; }
+#pragma unroll
+    for (int v = 0; v < NV; ++v) {
+      const float chunk_in = __shfl_sync(kFull, ex_v, v * Cfg::kWarps + warp);
+      const float carry_in = lflag[v] ? lval[v] : chunk_in + lval[v];
+      const int q0 = 4 * (v * NT + tid);
+      bool first = true;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if ((tails[v] >> e) & 1u) {
+          sm.out[b][q0 + e] = first ? carry_in + tv[v][e] : tv[v][e];
+          first = false;
+        }
+      }
+    }
+    (void)ex_f;
+    // this buffer's tail bits are no longer read: clear them for tile t+2
+    for (int w = tid; w < Cfg::kTailWords; w += NT) sm.tail[b][w] = 0u;
+    __syncthreads();
+
+    // (6) rows ending in this tile: y[r] = row sum within the tile (+ this CTA's carry for
+    //     the first row); coalesced stores (Alg.3 P:321 "y[row] <- running_total")
+    for (int r = tid; r < nrows; r += NT) {
+      const int e = sm.rowend[b][r];
+      const int s = r == 0 ? lo : sm.rowend[b][r - 1];
+      float yv = e > s ? sm.out[b][e - 1] : 0.f;
+      if (r == 0) yv += cta_carry;
+      a.y[i0 + r] = yv;
+    }
+    // (7) carry the open row (i1) to the next tile of this CTA (Alg.3)
+    cta_carry = nrows > 0 ? agg_val : cta_carry + agg_val;
+    i_last = i1;
+  }
+  if (tid == 0 && t_begin < t_end) {
+    a.carry_row[blockIdx.x] = i_last;
+    a.carry_val[blockIdx.x] = cta_carry;
+  }
+}
+
+// Fix-up (Alg.3): y[row] += carries of the CTAs whose runs ended inside `row`
+// (rows == rows means the terminal corner: skipped, reading R5).  Carries are sorted by row;
+// the first carry of each row sums its run in CTA order (deterministic).
+__global__ void fixup_kernel(int rows, int n, const int* __restrict__ carry_row,
+                             const float* __restrict__ carry_val, float* __restrict__ y) {
+  int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int r = carry_row[c];
+  if (r >= rows) return;
+  if (c > 0 && carry_row[c - 1] == r) return;
+  float s = 0.f;
+  for (int k = c; k < n && carry_row[k] == r; ++k) s += carry_val[k];
+  y[r] += s;
+}
+
+// ----------------------------------------------------------------------------- thread-mapped
+// Listing 3: for row in tiles() (grid-stride, Listing 2), for nz in
+// atoms(row): sum += values[nz] * x[indices[nz]]; y[row] = sum.  Four independent partial
+// sums (reading R12) for ILP.
+__global__ void __launch_bounds__(256) thread_mapped_kernel(int rows, const int* __restrict__ off,
+                                                            const int* __restrict__ col,
+                                                            const float* __restrict__ val,
+                                                            const float* __restrict__ x, float* __restrict__ y) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x) {
+    const int b = __ldg(off + r), e = __ldg(off + r + 1);
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    int k = b;
+    for (; k + 4 <= e; k += 4) {
+      s0 = fmaf(__ldg(val + k), ld_x(x + __ldg(col + k)), s0);
+      s1 = fmaf(__ldg(val + k + 1), ld_x(x + __ldg(col + k + 1)), s1);
+      s2 = fmaf(__ldg(val + k + 2), ld_x(x + __ldg(col + k + 2)), s2);
+      s3 = fmaf(__ldg(val + k + 3), ld_x(x + __ldg(col + k + 3)), s3);
+    }
+    for (; k < e; ++k) s0 = fmaf(__ldg(val + k), ld_x(x + __ldg(col + k)), s0);
+    y[r] = (s0 + s1) + (s2 + s3);
+  }
+}
+
+// ----------------------------------------------------------------------------- group-mapped
+// Alg.2 P:255-281 / P:1036-1041 with reading R8-R10: a group of G lanes takes G consecutive
+// rows per round; lane l loads its row's atom count, the group builds the inclusive prefix
+// sum, lanes stride the group's atom pool by G and find each atom's row with
+// a binary search in the prefix sum (get_tile); products are summed per row with a
+// warp segmented scan and accumulated in a per-warp, per-row shared-memory slot (no
+// atomics, deterministic); y[row] = sum over the group's warps in fixed order.
+template <int G>
+__global__ void __launch_bounds__(256) group_mapped_kernel(int rows, const int* __restrict__ off,
+                                                           const int* __restrict__ col,
+                                                           const float* __restrict__ val,
+                                                           const float* __restrict__ x, float* __restrict__ y) {
+  constexpr int NT = 256;
+  constexpr int kGroups = NT / G;
+  constexpr int kWpg = G / 32;  // warps per group
+  __shared__ int s_incl[kGroups][G];
+  __shared__ int s_start[kGroups][G];
+  __shared__ float s_acc[NT / 32][G];
+  __shared__ int s_wsum[NT / 32];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = tid / G, gl = tid % G, wig = gl >> 5;  // group, lane in group, warp in group
+  const int64_t n_groups = (int64_t)gridDim.x * kGroups;
+
+  for (int64_t base = (blockIdx.x * (int64_t)kGroups + grp) * G; base < rows; base += n_groups * G) {
+    // all groups of the CTA run the same number of rounds (uniform loop for __syncthreads)
+    const int64_t r = base + gl;
+    const int b = r < rows ? __ldg(off + r) : 0;
+    const int cnt = r < rows ? __ldg(off + r + 1) - b : 0;
+    int incl = warp_incl_scan_int(cnt, lane);
+    if (kWpg > 1) {
+      if (lane == 31) s_wsum[warp] = incl;
+      __syncthreads();
+      int add = 0;
+      for (int w = 0; w < wig; ++w) add += s_wsum[grp * kWpg + w];
+      incl += add;
+    }
+    s_incl[grp][gl] = incl;
+    s_start[grp][gl] = b;
+    for (int q = lane; q < G; q += 32) s_acc[warp][q] = 0.f;
+    if (kWpg > 1) __syncthreads(); else __syncwarp();
+    const int total = s_incl[grp][G - 1];
+
+    // this warp takes atoms k = k0 + 32*wig + lane, k0 += G
+    for (int k0 = 0; k0 < total; k0 += G) {
+      const int k = k0 + 32 * wig + lane;
+      const bool ok = k < total;
+      int rl = 0;
+      float p = 0.f;
+      if (ok) {
+        int lo = 0, hi = G - 1;  // first rl with incl[rl] > k
+        while (lo < hi) {
+          int mid = (lo + hi) >> 1;
+          if (s_incl[grp][mid] > k) hi = mid; else lo = mid + 1;
+        }
+        rl = lo;
+        const int excl = rl ? s_incl[grp][rl - 1] : 0;
+        const int nz = s_start[grp][rl] + (k - excl);
+        p = __ldg(val + nz) * ld_x(x + __ldg(col + nz));
+      }
+      const int prev = __shfl_up_sync(kFull, rl, 1);
+      const int next = __shfl_down_sync(kFull, rl, 1);
+      const bool next_ok = __shfl_down_sync(kFull, (int)ok, 1);
+      bool head = lane == 0 || prev != rl;
+      float v = p;
+      warp_segscan_incl(head, v, lane);
+      const bool tail = ok && (lane == 31 || !next_ok || next != rl);
+      if (tail) s_acc[warp][rl] += v;
+      __syncwarp();
+    }
+    if (kWpg > 1) __syncthreads(); else __syncwarp();
+    if (r < rows) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < kWpg; ++w) s += s_acc[grp * kWpg + w][gl];
+      y[r] = s;
+    }
+    if (kWpg > 1) __syncthreads(); else __syncwarp();
+  }
+}
+
+}  // namespace lbk

@@ -1,0 +1,308 @@
+"""Thin ctypes binding over liblb.so (include/lb.h).  Argument marshalling only: every step of
+the SpMV path runs in the library's CUDA kernels; there is no Python or CPU fallback, and a
+missing/unloadable library raises immediately.
+
+PyTorch is used for device memory and streams only.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_ROOT = os.path.dirname(_PKG)
+LIB_PATH = os.path.join(_PKG, "liblb.so")
+HEADER = os.path.join(_ROOT, "include", "lb.h")
+
+LB_OK, LB_ERR_INVALID_ARG, LB_ERR_INVALID_CSR, LB_ERR_UNSUPPORTED, LB_ERR_OOM, LB_ERR_CUDA, LB_ERR_NCCL = range(7)
+SCHEDULES = {"thread_mapped": 0, "group_mapped": 1, "merge_path": 2, "block_mapped": 3}
+LB_SPMV_REPARTITION = 1
+DEFAULT_ITEMS_PER_TILE = 2048
+
+
+class LbError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"liblb status {status}: {msg}")
+        self.status = status
+
+
+class InvalidCsr(LbError, ValueError):
+    pass
+
+
+_lib = None
+
+
+def declared_functions() -> list[str]:
+    """Names of every function include/lb.h declares."""
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(lb_[a-z_0-9]+)\s*\(", src, flags=re.M)))
+
+
+def lib() -> ctypes.CDLL:
+    """Load liblb.so (fails loudly if it is missing; build it with paper_2212_08964_b200.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_2212_08964_b200.build` "
+                           "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    i32, i64, u32, p, sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_size_t
+    st = ctypes.c_int
+    sig = {
+        "lb_csr_create": ([i64, i64, i64, p, p, p, i32, p, ctypes.POINTER(p)], st),
+        "lb_csr_destroy": ([p], st),
+        "lb_csr_set_items_per_tile": ([p, i32], st),
+        "lb_partition_size": ([p, i32, ctypes.POINTER(i64)], st),
+        "lb_partition": ([p, i32, p, p], st),
+        "lb_spmv": ([p, ctypes.c_int, p, p, p], st),
+        "lb_spmv_ex": ([p, ctypes.c_int, p, p, u32, p], st),
+        "lb_spmv_host_workspace_size": ([i64, i64, i64], sz),
+        "lb_spmv_host": ([i64, i64, i64, p, p, p, p, p, ctypes.c_int, p, sz, p], st),
+        "lb_spmv_phase_times": ([p, ctypes.c_int, p, p, p, ctypes.POINTER(ctypes.c_float)], st),
+        "lb_shard_bounds": ([p, i64, i32, p], st),
+        "lb_comm_unique_id": ([p], st),
+        "lb_comm_init": ([p, i32, i32, i32, ctypes.POINTER(p)], st),
+        "lb_comm_destroy": ([p], st),
+        "lb_spmv_multi": ([p, p, ctypes.c_int, p, p, p, p], st),
+        "lb_allgather_rows": ([p, p, p, p], st),
+        "lb_last_error": ([], ctypes.c_char_p),
+        "lb_launch_count": ([], ctypes.c_uint64),
+        "lb_version": ([], ctypes.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != LB_OK:
+        msg = lib().lb_last_error().decode()
+        if status == LB_ERR_INVALID_CSR:
+            raise InvalidCsr(status, msg)
+        raise LbError(status, msg)
+
+
+def last_error() -> str:
+    return lib().lb_last_error().decode()
+
+
+def launch_count() -> int:
+    return int(lib().lb_launch_count())
+
+
+def version() -> str:
+    return lib().lb_version().decode()
+
+
+def _stream(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _sched(schedule) -> int:
+    if isinstance(schedule, int):
+        return schedule
+    try:
+        return SCHEDULES[schedule]
+    except KeyError:
+        raise ValueError(f"unknown schedule {schedule!r}; one of {sorted(SCHEDULES)}") from None
+
+
+def _dev_tensor(t: torch.Tensor, dtype, name: str, n: int | None = None) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or t.device.type != "cuda":
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if n is not None and t.numel() != n:
+        raise ValueError(f"{name} has {t.numel()} elements, expected {n}")
+    return t
+
+
+class CsrMatrix:
+    """A borrowed CSR matrix on the GPU (lb_csr_t).  Keeps references to its tensors so they
+    outlive the handle (include/lb.h ownership rule)."""
+
+    def __init__(self, rows: int, cols: int, row_offsets: torch.Tensor, col_idx: torch.Tensor,
+                 values: torch.Tensor, validate: bool = True, stream=None):
+        self.rows, self.cols = int(rows), int(cols)
+        self.row_offsets = _dev_tensor(row_offsets, torch.int32, "row_offsets", self.rows + 1)
+        self.col_idx = _dev_tensor(col_idx, torch.int32, "col_idx")
+        self.values = _dev_tensor(values, torch.float32, "values", self.col_idx.numel())
+        self.nnz = int(self.col_idx.numel())
+        self._h = ctypes.c_void_p()
+        with torch.cuda.device(self.row_offsets.device):
+            _check(lib().lb_csr_create(self.rows, self.cols, self.nnz, self.row_offsets.data_ptr(),
+                                       self.col_idx.data_ptr() if self.nnz else None,
+                                       self.values.data_ptr() if self.nnz else None, int(bool(validate)),
+                                       _stream(stream), ctypes.byref(self._h)))
+        self.device = self.row_offsets.device
+        self.items_per_tile = DEFAULT_ITEMS_PER_TILE
+
+    @classmethod
+    def from_csr(cls, A, device="cuda", validate: bool = True) -> "CsrMatrix":
+        """From any object with rows, cols, row_offsets, col_idx, values (e.g. lbgen.Csr)."""
+        return cls(A.rows, A.cols, A.row_offsets.to(device), A.col_idx.to(device), A.values.to(device),
+                   validate=validate)
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        if not self._h:
+            raise ValueError("CsrMatrix is closed")
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().lb_csr_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_items_per_tile(self, L: int):
+        _check(lib().lb_csr_set_items_per_tile(self.handle, int(L)))
+        self.items_per_tile = int(L) or DEFAULT_ITEMS_PER_TILE
+
+    def num_tiles(self, items_per_tile: int = 0) -> int:
+        n = ctypes.c_int64()
+        _check(lib().lb_partition_size(self.handle, int(items_per_tile), ctypes.byref(n)))
+        return int(n.value)
+
+    def partition(self, items_per_tile: int = 0, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Merge-path tile coordinates, int32 [T+1, 2] of (row, nz) (lb_partition)."""
+        T = self.num_tiles(items_per_tile)
+        if out is None:
+            out = torch.empty((T + 1, 2), dtype=torch.int32, device=self.device)
+        _dev_tensor(out, torch.int32, "out", 2 * (T + 1))
+        _check(lib().lb_partition(self.handle, int(items_per_tile), out.data_ptr(), _stream(stream)))
+        return out
+
+    def spmv(self, x: torch.Tensor, y: torch.Tensor | None = None, schedule="merge_path",
+             repartition: bool = False, stream=None) -> torch.Tensor:
+        """y = A x (lb_spmv / lb_spmv_ex)."""
+        _dev_tensor(x, torch.float32, "x", self.cols)
+        if y is None:
+            y = torch.empty(self.rows, dtype=torch.float32, device=self.device)
+        _dev_tensor(y, torch.float32, "y", self.rows)
+        flags = LB_SPMV_REPARTITION if repartition else 0
+        _check(lib().lb_spmv_ex(self.handle, _sched(schedule), x.data_ptr() if self.cols else None,
+                                y.data_ptr() if self.rows else None, flags, _stream(stream)))
+        return y
+
+    def phase_times(self, x: torch.Tensor, y: torch.Tensor, schedule="merge_path", stream=None) -> list[float]:
+        """[partition, main, fixup] milliseconds of one call (lb_spmv_phase_times)."""
+        ms = (ctypes.c_float * 3)()
+        _check(lib().lb_spmv_phase_times(self.handle, _sched(schedule), x.data_ptr(), y.data_ptr(),
+                                         _stream(stream), ms))
+        return [float(v) for v in ms]
+
+
+def spmv(A: CsrMatrix, x: torch.Tensor, schedule="merge_path", y=None) -> torch.Tensor:
+    return A.spmv(x, y, schedule)
+
+
+# ----------------------------------------------------------------------------- end to end (host buffers)
+
+class HostSpmv:
+    """End-to-end y = A x from host (pinned) buffers through lb_spmv_host: H2D copies of the
+    CSR arrays and x, partition + SpMV, D2H copy of y, all inside the call."""
+
+    def __init__(self, rows: int, cols: int, nnz: int, device="cuda"):
+        self.rows, self.cols, self.nnz = rows, cols, nnz
+        self.ws_bytes = int(lib().lb_spmv_host_workspace_size(rows, cols, nnz))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=device)
+
+    def __call__(self, row_offsets: torch.Tensor, col_idx: torch.Tensor, values: torch.Tensor, x: torch.Tensor,
+                 y: torch.Tensor, schedule="merge_path", stream=None) -> torch.Tensor:
+        for t, name in ((row_offsets, "row_offsets"), (col_idx, "col_idx"), (values, "values"), (x, "x"), (y, "y")):
+            if t.device.type != "cpu" or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous host tensor")
+        with torch.cuda.device(self.ws.device):
+            _check(lib().lb_spmv_host(self.rows, self.cols, self.nnz, row_offsets.data_ptr(), col_idx.data_ptr(),
+                                      values.data_ptr(), x.data_ptr(), y.data_ptr(), _sched(schedule),
+                                      self.ws.data_ptr(), self.ws_bytes, _stream(stream)))
+        return y
+
+
+# ----------------------------------------------------------------------------- multi-GPU host logic
+
+def shard_bounds(row_offsets, nranks: int) -> np.ndarray:
+    """Equal-nnz row-shard bounds (lb_shard_bounds, host-only)."""
+    off = row_offsets.detach().cpu().numpy() if hasattr(row_offsets, "detach") else np.asarray(row_offsets)
+    off = np.ascontiguousarray(off, dtype=np.int32)
+    out = np.empty(nranks + 1, np.int64)
+    _check(lib().lb_shard_bounds(off.ctypes.data, off.size - 1, int(nranks), out.ctypes.data))
+    return out
+
+
+def shard_csr(row_offsets: torch.Tensor, col_idx: torch.Tensor, values: torch.Tensor, bounds, rank: int):
+    """Rows [b_r, b_{r+1}) of a CSR as its own CSR (offsets rebased to 0, global column ids).
+    Returns fresh contiguous tensors on the same device (so 16-byte alignment holds)."""
+    b0, b1 = int(bounds[rank]), int(bounds[rank + 1])
+    off = row_offsets[b0:b1 + 1].to(torch.int64)
+    base = int(off[0]) if off.numel() else 0
+    end = int(off[-1]) if off.numel() else 0
+    return ((off - base).to(torch.int32).contiguous(), col_idx[base:end].clone(), values[base:end].clone())
+
+
+class Comm:
+    """NCCL communicator owned by liblb (lb_comm_t)."""
+
+    def __init__(self, uid: bytes, rank: int, nranks: int, device: int):
+        self.rank, self.nranks, self.device = rank, nranks, device
+        self._c = ctypes.c_void_p()
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        _check(lib().lb_comm_init(buf, rank, nranks, device, ctypes.byref(self._c)))
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = (ctypes.c_uint8 * 128)()
+        _check(lib().lb_comm_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def from_process_group(cls, device: int) -> "Comm":
+        """Bootstrap over torch.distributed (any backend): rank 0 makes the id, all ranks join."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls(obj[0], rank, world, device)
+
+    def close(self):
+        if getattr(self, "_c", None):
+            lib().lb_comm_destroy(self._c)
+            self._c = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def spmv_multi(self, A_local: CsrMatrix, bounds, x_full: torch.Tensor, y_full: torch.Tensor,
+                   schedule="merge_path", stream=None) -> torch.Tensor:
+        b = np.ascontiguousarray(bounds, dtype=np.int64)
+        _check(lib().lb_spmv_multi(A_local.handle, self._c, _sched(schedule), b.ctypes.data, x_full.data_ptr(),
+                                   y_full.data_ptr(), _stream(stream)))
+        return y_full
+
+    def allgather_rows(self, bounds, y_full: torch.Tensor, stream=None) -> torch.Tensor:
+        b = np.ascontiguousarray(bounds, dtype=np.int64)
+        _check(lib().lb_allgather_rows(self._c, b.ctypes.data, y_full.data_ptr(), _stream(stream)))
+        return y_full

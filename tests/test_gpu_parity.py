@@ -1,0 +1,370 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, element by element.
+
+Bars (BASELINE.json north_star):
+  * partition coordinates: bit-exact;
+  * y in integer mode (values {+-1,+-2}, x {-4..4}, every partial sum an exact fp32 integer):
+    bit-exact, compared by value;
+  * y in tolerance mode (values and x uniform in [-1,1) on a 2^-23 grid):
+    |y_gpu - y_ref| <= 1e-5 * s_ref + 1e-30 per row, s_ref = sum_k |a_ik x_k|.
+Sizes span several tiles and ragged tails; full BASELINE.json sizes are covered by
+test_full_size_configs (partition bit-exact on every tile, y on every row for C1-C4 and on
+sampled rows for C5).
+"""
+import numpy as np
+import pytest
+import torch
+
+import lbgen
+import oracle
+import paper_2212_08964_b200 as lb
+
+pytestmark = pytest.mark.gpu
+
+SCHEDS = ["merge_path", "thread_mapped", "group_mapped", "block_mapped"]
+TOL = 1e-5
+
+
+def ref(A: lbgen.Csr, x: torch.Tensor):
+    return oracle.spmv(A.row_offsets, A.col_idx, A.values, x, threads=A.nnz > 1_000_000)
+
+
+def check_y(y_gpu: torch.Tensor, y_ref: np.ndarray, s_ref: np.ndarray, exact: bool, what=""):
+    y = y_gpu.detach().double().cpu().numpy()
+    assert y.shape == y_ref.shape
+    if exact:
+        bad = np.nonzero(y != y_ref)[0]
+        assert bad.size == 0, f"{what}: {bad.size} rows differ, first {bad[:5]} gpu={y[bad[:5]]} ref={y_ref[bad[:5]]}"
+    else:
+        err = np.abs(y - y_ref)
+        lim = TOL * s_ref + 1e-30
+        bad = np.nonzero(err > lim)[0]
+        assert bad.size == 0, f"{what}: {bad.size} rows out of tolerance, worst rel {np.max(err / (s_ref + 1e-30)):.3e}"
+
+
+def run(A: lbgen.Csr, x: torch.Tensor, sched: str, L: int = 0) -> torch.Tensor:
+    M = lb.CsrMatrix.from_csr(A)
+    if L:
+        M.set_items_per_tile(L)
+    y = torch.full((A.rows,), float("nan"), device="cuda")
+    M.spmv(x.cuda(), y, sched)
+    torch.cuda.synchronize()
+    return y
+
+
+def random_csr(rng, rows, cols, max_len, p_empty, vmode):
+    lens = rng.integers(0, max_len + 1, rows)
+    lens[rng.random(rows) < p_empty] = 0
+    off = np.zeros(rows + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    nnz = int(off[-1])
+    col = np.sort(rng.integers(0, max(cols, 1), nnz))  # per-row order is irrelevant to SpMV
+    val = rng.choice([-2.0, -1.0, 1.0, 2.0], nnz) if vmode == "int" else rng.integers(-(1 << 23), 1 << 23, nnz) * 2.0 ** -23
+    return lbgen.Csr(rows, cols, torch.tensor(off, dtype=torch.int32), torch.tensor(col, dtype=torch.int32),
+                     torch.tensor(val, dtype=torch.float32))
+
+
+SMALL = {
+    "rmat12": lambda vm: lbgen.rmat(12, 16, 3, vm),
+    "rmat14": lambda vm: lbgen.rmat(14, 8, 7, vm),
+    "stencil100": lambda vm: lbgen.stencil(100, 2, vm),
+    "skewed": lambda vm: lbgen.skewed(1 << 13, 5, 20_000, 50_000, 4, vm),
+    "c1": lambda vm: lbgen.make_config("c1", vm),
+    "uniform_rows": lambda vm: lbgen.uniform_rows(13, 16, 6, vm),
+}
+
+
+# ---------------------------------------------------------------- partition (bit-exact)
+
+@pytest.mark.parametrize("L", [1, 2, 3, 7, 256, 1024, 2048, 5000])
+@pytest.mark.parametrize("name", ["rmat12", "stencil100", "skewed", "c1"])
+def test_partition_bit_exact(name, L):
+    A = SMALL[name]("int")
+    M = lb.CsrMatrix.from_csr(A)
+    got = M.partition(L).cpu().numpy()
+    want = oracle.partition(A.row_offsets, L)
+    assert np.array_equal(got, want)
+
+
+def test_partition_random_every_diagonal():
+    rng = np.random.default_rng(1)
+    for trial in range(40):
+        A = random_csr(rng, int(rng.integers(1, 300)), 50, int(rng.integers(0, 30)), float(rng.random()), "int")
+        M = lb.CsrMatrix.from_csr(A)
+        assert np.array_equal(M.partition(1).cpu().numpy(), oracle.partition(A.row_offsets, 1)), trial
+
+
+# ---------------------------------------------------------------- SpMV parity
+
+@pytest.mark.parametrize("sched", SCHEDS)
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_spmv_integer_exact(name, sched):
+    A = SMALL[name]("int")
+    x = lbgen.make_x(A.cols, "int", 11)
+    y_ref, s_ref = ref(A, x)
+    assert np.all(s_ref < 2 ** 24)
+    check_y(run(A, x, sched), y_ref, s_ref, True, f"{name}/{sched}")
+
+
+@pytest.mark.parametrize("sched", SCHEDS)
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_spmv_tolerance(name, sched):
+    A = SMALL[name]("float")
+    x = lbgen.make_x(A.cols, "float", 12)
+    y_ref, s_ref = ref(A, x)
+    check_y(run(A, x, sched), y_ref, s_ref, False, f"{name}/{sched}")
+
+
+@pytest.mark.parametrize("L", [1024, 2048])
+@pytest.mark.parametrize("vmode", ["int", "float"])
+def test_merge_path_tile_lengths(L, vmode):
+    A = lbgen.rmat(13, 16, 5, vmode)
+    x = lbgen.make_x(A.cols, vmode, 3)
+    y_ref, s_ref = ref(A, x)
+    check_y(run(A, x, "merge_path", L), y_ref, s_ref, vmode == "int")
+
+
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_random_ragged_matrices(sched):
+    rng = np.random.default_rng(5)
+    for trial in range(25):
+        rows = int(rng.integers(1, 3000))
+        A = random_csr(rng, rows, int(rng.integers(1, 500)), int(rng.integers(0, 60)), float(rng.random()) * 0.7, "int")
+        x = lbgen.make_x(A.cols, "int", trial)
+        y_ref, s_ref = ref(A, x)
+        check_y(run(A, x, sched), y_ref, s_ref, True, f"trial {trial}")
+
+
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_identity_and_diagonal_bit_exact(sched):
+    n = 70_001
+    idx = torch.arange(n, dtype=torch.int32)
+    off = torch.arange(n + 1, dtype=torch.int32)
+    x = lbgen.make_x(n, "float", 1)
+    I = lbgen.Csr(n, n, off, idx, torch.ones(n))
+    assert torch.equal(run(I, x, sched).cpu(), x)                       # y = x
+    d = lbgen.make_x(n, "float", 2)
+    D = lbgen.Csr(n, n, off, idx, d)
+    assert torch.equal(run(D, x, sched).cpu(), d * x)                   # y_i = fl(d_i x_i)
+
+
+@pytest.mark.parametrize("sched", SCHEDS)
+@pytest.mark.parametrize("xmode", ["ones", "index"])
+def test_stencil_closed_form(sched, xmode):
+    N = 300
+    A = lbgen.stencil(N, 2, "stencil")
+    x = lbgen.make_x(N * N, xmode, 0)
+    i = np.arange(N * N, dtype=np.int64)
+    yy, xx = i // N, i % N
+    missing = [(yy == 0, i - N), (xx == 0, i - 1), (xx == N - 1, i + 1), (yy == N - 1, i + N)]
+    if xmode == "ones":
+        expect = sum(m.astype(np.float64) for m, _ in missing)
+    else:
+        expect = sum(np.where(m, v, 0).astype(np.float64) for m, v in missing)
+    y = run(A, x, sched).double().cpu().numpy()
+    assert np.array_equal(y, expect)
+
+
+# ---------------------------------------------------------------- edge cases
+
+def _csr(off, cols, col=None, val=None):
+    off = torch.tensor(off, dtype=torch.int32)
+    nnz = int(off[-1])
+    col = torch.zeros(nnz, dtype=torch.int32) if col is None else torch.tensor(col, dtype=torch.int32)
+    val = torch.ones(nnz) if val is None else torch.tensor(val, dtype=torch.float32)
+    return lbgen.Csr(off.numel() - 1, cols, off, col, val)
+
+
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_edge_cases(sched):
+    cases = {
+        "no_nnz": _csr([0] * 5001, 3),
+        "one_giant_row": _csr([0, 200_003], 1),
+        "giant_last_row": _csr([0] * 3000 + [100_000], 1),
+        "empty_rows_between": _csr([0, 1, 1, 1, 5, 5, 9], 1),
+        "golden": _csr([0, 1, 3, 3, 6], 1),
+        "single": _csr([0, 1], 1),
+        "cols1_many_rows": _csr(list(range(0, 2 * 40_000 + 1, 2)), 1),
+    }
+    for name, A in cases.items():
+        x = torch.full((A.cols,), 1.0)
+        y_ref, s_ref = ref(A, x)
+        check_y(run(A, x, sched), y_ref, s_ref, True, name)
+    # golden example: y = [1, 2, 0, 3]
+    assert run(cases["golden"], torch.ones(1), sched).tolist() == [1, 2, 0, 3]
+
+
+def test_empty_matrix_is_noop():
+    M = lb.CsrMatrix(0, 0, torch.zeros(1, dtype=torch.int32, device="cuda"),
+                     torch.zeros(0, dtype=torch.int32, device="cuda"), torch.zeros(0, device="cuda"))
+    y = torch.zeros(0, device="cuda")
+    for s in SCHEDS:
+        M.spmv(torch.zeros(0, device="cuda"), y, s)
+    assert M.partition(16).cpu().tolist() == [[0, 0]]
+
+
+def test_unaligned_arrays_use_scalar_path():
+    A = lbgen.rmat(12, 8, 9, "int")
+    x = lbgen.make_x(A.cols, "int", 4)
+    y_ref, s_ref = ref(A, x)
+    # shift col/val by one element inside a larger buffer -> not 16-byte aligned
+    colbuf = torch.zeros(A.nnz + 1, dtype=torch.int32, device="cuda")
+    valbuf = torch.zeros(A.nnz + 1, device="cuda")
+    colbuf[1:] = A.col_idx.cuda()
+    valbuf[1:] = A.values.cuda()
+    M = lb.CsrMatrix(A.rows, A.cols, A.row_offsets.cuda(), colbuf[1:], valbuf[1:])
+    y = M.spmv(x.cuda())
+    check_y(y, y_ref, s_ref, True, "unaligned")
+
+
+def test_validation_rejects_invalid_csr():
+    dev = "cuda"
+    with pytest.raises(lb.InvalidCsr, match="monotone at row 1"):
+        lb.CsrMatrix(3, 4, torch.tensor([0, 2, 1, 3], dtype=torch.int32, device=dev),
+                     torch.zeros(3, dtype=torch.int32, device=dev), torch.ones(3, device=dev))
+    with pytest.raises(lb.InvalidCsr, match=r"col_idx\[2\]"):
+        lb.CsrMatrix(2, 4, torch.tensor([0, 1, 3], dtype=torch.int32, device=dev),
+                     torch.tensor([0, 3, 4], dtype=torch.int32, device=dev), torch.ones(3, device=dev))
+    with pytest.raises(lb.InvalidCsr, match=r"row_offsets\[0\]"):
+        lb.CsrMatrix(2, 4, torch.tensor([1, 1, 3], dtype=torch.int32, device=dev),
+                     torch.zeros(3, dtype=torch.int32, device=dev), torch.ones(3, device=dev))
+    with pytest.raises(lb.InvalidCsr, match="!= nnz"):
+        lb.CsrMatrix(2, 4, torch.tensor([0, 1, 2], dtype=torch.int32, device=dev),
+                     torch.zeros(3, dtype=torch.int32, device=dev), torch.ones(3, device=dev))
+
+
+def test_argument_errors():
+    A = lbgen.make_config("c1", "int")
+    M = lb.CsrMatrix.from_csr(A)
+    x = torch.ones(A.cols, device="cuda")
+    with pytest.raises(ValueError):
+        M.spmv(x, schedule="nonsense")
+    with pytest.raises(lb.LbError):
+        M.spmv(x, schedule=17)
+    with pytest.raises(lb.LbError):
+        M.set_items_per_tile(3000)
+    with pytest.raises(ValueError):
+        M.spmv(torch.ones(A.cols + 1, device="cuda"))
+
+
+def test_deterministic_bitwise():
+    A = lbgen.rmat(14, 16, 2, "float")
+    x = lbgen.make_x(A.cols, "float", 8).cuda()
+    M = lb.CsrMatrix.from_csr(A)
+    for sched in SCHEDS:
+        y1 = M.spmv(x, schedule=sched, repartition=True).clone()
+        y2 = M.spmv(x, schedule=sched).clone()
+        assert torch.equal(y1, y2)
+
+
+def test_launch_count_and_phase_times():
+    A = lbgen.rmat(12, 16, 2, "float")
+    M = lb.CsrMatrix.from_csr(A)
+    x = lbgen.make_x(A.cols, "float", 8).cuda()
+    y = torch.empty(A.rows, device="cuda")
+    n0 = lb.launch_count()
+    M.spmv(x, y, "merge_path", repartition=True)
+    assert lb.launch_count() - n0 == 3          # partition + tiles + fix-up
+    ms = M.phase_times(x, y, "merge_path")
+    assert len(ms) == 3 and all(v >= 0 for v in ms) and ms[1] > 0
+
+
+# ---------------------------------------------------------------- end to end + multi-GPU layer
+
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_spmv_host_end_to_end(sched):
+    A = lbgen.rmat(13, 16, 4, "int")
+    x = lbgen.make_x(A.cols, "int", 5)
+    y_ref, s_ref = ref(A, x)
+    h = lb.HostSpmv(A.rows, A.cols, A.nnz)
+    y = torch.empty(A.rows).pin_memory()
+    h(A.row_offsets.pin_memory(), A.col_idx.pin_memory(), A.values.pin_memory(), x.pin_memory(), y, sched)
+    check_y(y, y_ref, s_ref, True, "host")
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_row_shards_concatenate_bit_identical(G):
+    """G equal-nnz shards run one after another on one GPU, concatenated,
+    equal the single-GPU y bit for bit in integer mode."""
+    A = lbgen.rmat(13, 16, 6, "int")
+    x = lbgen.make_x(A.cols, "int", 6).cuda()
+    full = run(A, x.cpu(), "merge_path")
+    b = lb.shard_bounds(A.row_offsets, G)
+    ys = []
+    for r in range(G):
+        off, col, val = lb.shard_csr(A.row_offsets.cuda(), A.col_idx.cuda(), A.values.cuda(), b, r)
+        M = lb.CsrMatrix(int(b[r + 1] - b[r]), A.cols, off, col, val)
+        ys.append(M.spmv(x))
+    assert torch.equal(torch.cat(ys), full)
+
+
+def test_spmv_multi_single_rank_nccl():
+    A = lbgen.rmat(12, 16, 6, "int")
+    x = lbgen.make_x(A.cols, "int", 6)
+    y_ref, s_ref = ref(A, x)
+    uid = lb.Comm.unique_id()
+    comm = lb.Comm(uid, 0, 1, torch.cuda.current_device())
+    b = lb.shard_bounds(A.row_offsets, 1)
+    M = lb.CsrMatrix.from_csr(A)
+    y = torch.empty(A.rows, device="cuda")
+    comm.spmv_multi(M, b, x.cuda(), y)
+    torch.cuda.synchronize()
+    check_y(y, y_ref, s_ref, True, "multi")
+    comm.close()
+
+
+# ---------------------------------------------------------------- full BASELINE.json sizes
+
+def _sample_rows(A_dev: lbgen.Csr, coords: np.ndarray, n_random: int, seed: int) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    rows = A_dev.rows
+    tile_rows = np.unique(np.clip(coords[:, 0].astype(np.int64), 0, rows - 1))
+    lens = (A_dev.row_offsets[1:] - A_dev.row_offsets[:-1])
+    top = torch.topk(lens, min(64, rows)).indices.cpu().numpy()
+    pick = np.concatenate([rng.integers(0, rows, n_random), tile_rows[:: max(1, tile_rows.size // 20000)], top,
+                           [0, rows - 1]])
+    return np.unique(pick)
+
+
+def _packed(A_dev: lbgen.Csr, sel: np.ndarray):
+    off = A_dev.row_offsets.to(torch.int64)
+    s = torch.as_tensor(sel, device=off.device)
+    b, e = off[s], off[s + 1]
+    lens = e - b
+    so = torch.zeros(sel.size + 1, dtype=torch.int64, device=off.device)
+    so[1:] = torch.cumsum(lens, 0)
+    idx = torch.repeat_interleave(b - so[:-1], lens) + torch.arange(int(so[-1]), device=off.device)
+    return so.cpu(), A_dev.col_idx[idx].cpu(), A_dev.values[idx].cpu()
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c5"])
+def test_full_size_configs(cfg):
+    """Every schedule at the BASELINE.json size of each config (merge-path at the launch
+    configuration bench.py times): partition bit-exact on every tile; integer mode bit-exact on
+    every row (C1-C4) or on sampled rows (C5); tolerance mode on sampled rows."""
+    torch.cuda.empty_cache()
+    scheds = SCHEDS if cfg != "c5" else ["merge_path", "group_mapped"]
+    for vmode in ("int", "float"):
+        A = lbgen.make_config(cfg, vmode, device="cuda")
+        x = lbgen.x_for_config(cfg, A.cols, vmode, device="cuda")
+        M = lb.CsrMatrix.from_csr(A, device="cuda")
+        if vmode == "int":
+            coords = M.partition().cpu().numpy()
+            assert np.array_equal(coords, oracle.partition(A.row_offsets.cpu(), 2048)), "partition"
+        else:
+            coords = M.partition().cpu().numpy()
+        full = vmode == "int" and cfg != "c5"
+        if full:
+            y_ref, s_ref = oracle.spmv(A.row_offsets.cpu(), A.col_idx.cpu(), A.values.cpu(), x.cpu(), threads=True)
+            sel = None
+        else:
+            sel = _sample_rows(A, coords, 20_000, 1)
+            so, sc, sv = _packed(A, sel)
+            y_ref, s_ref = oracle.spmv_packed(so, sc, sv, x.cpu())
+        for sched in scheds:
+            y = torch.full((A.rows,), float("nan"), device="cuda")
+            M.spmv(x, y, sched, repartition=True)
+            torch.cuda.synchronize()
+            yy = y if sel is None else y[torch.as_tensor(sel, device="cuda")]
+            check_y(yy, y_ref, s_ref, vmode == "int", f"{cfg}/{vmode}/{sched}")
+        del M, A, x
+        torch.cuda.empty_cache()
