@@ -41,7 +41,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=None, help="c1..c6 (default: c3 at N=1, c5 at N>1)")
     ap.add_argument("--schedule", default="merge_path")
-    ap.add_argument("--items-per-tile", type=int, default=2048)
+    ap.add_argument("--items-per-tile", type=int, default=0, help="merge-path tile length L (0: library default)")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / cpu_baseline / clocks (profiling runs)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="budget for the cpu_baseline sample")
@@ -198,6 +198,7 @@ def run_single(args, cfg):
     rows, cols, nnz = A.rows, A.cols, A.nnz
     M = lb.CsrMatrix.from_csr(A, device=dev, validate=True)
     M.set_items_per_tile(args.items_per_tile)
+    args.items_per_tile = M.items_per_tile
     y = torch.empty(rows, device=dev)
     stream = torch.cuda.current_stream()
     sched = args.schedule

@@ -12,6 +12,7 @@
 #include <climits>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -48,11 +49,23 @@ lb_status_t fail(lb_status_t st, const char* fmt, ...) {
 
 constexpr int kNT = 256;
 constexpr int kMaxCtas = 8192;      // carry slots per handle (>= SMs x resident CTAs)
-constexpr int kMinTile = 1024;      // smallest supported L: sizes the partition cache
+constexpr int kMinTile = 1016;      // smallest supported L: sizes the partition cache
+
+// Merge-path tile lengths: L = 256*E - 8 for E nonzeros per thread (see PipeCfg).
+constexpr int kNumL = 4;
+constexpr int kE[kNumL] = {4, 8, 12, 16};
+constexpr int kPipeStages = 2;
+inline int l_of(int e) { return kNT * e - 8; }
+inline int l_index(int L) {
+  for (int i = 0; i < kNumL; ++i)
+    if (l_of(kE[i]) == L) return i;
+  return -1;
+}
 
 struct DeviceInfo {
   int sm_count = 0;
-  int grid_1024 = 0, grid_2048 = 0;  // persistent grid of the merge-path kernel per L
+  int fb_grid[kNumL] = {0};    // persistent grid of the fallback (unaligned) merge kernel per L
+  int pipe_grid[kNumL] = {0};  // persistent grid of the TMA-pipelined merge kernel per L
 };
 
 DeviceInfo g_dev[64];
@@ -61,14 +74,25 @@ std::mutex g_dev_mu;
 using stream_t = cudaStream_t;
 inline stream_t S(void* s) { return reinterpret_cast<stream_t>(s); }
 
-template <int L, bool VEC>
-size_t merge_smem() { return sizeof(typename lbk::MergeCfg<kNT, L, VEC>::Smem); }
+template <int E>
+size_t pipe_smem() { return sizeof(typename lbk::PipeCfg<kNT, E, kPipeStages>::Smem); }
+template <int E>
+size_t fb_smem() { return sizeof(typename lbk::MergeCfg<kNT, kNT * E - 8, true>::Smem); }
 
-template <int L, bool VEC>
-lb_status_t merge_prepare(int* blocks_per_sm) {
-  auto k = lbk::merge_tile_kernel<kNT, L, VEC>;
-  LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)merge_smem<L, VEC>()));
-  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k, kNT, merge_smem<L, VEC>()));
+template <int E>
+lb_status_t prepare_e(int* pipe_blocks, int* fb_blocks) {
+  auto kp = lbk::merge_pipe_kernel<kNT, E, kPipeStages>;
+  LB_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem<E>()));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(pipe_blocks, kp, kNT, pipe_smem<E>()));
+  constexpr int L = kNT * E - 8;
+  auto k1 = lbk::merge_tile_kernel<kNT, L, true>;
+  auto k2 = lbk::merge_tile_kernel<kNT, L, false>;
+  int b1 = 0, b2 = 0;
+  LB_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb_smem<E>()));
+  LB_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb_smem<E>()));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k1, kNT, fb_smem<E>()));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2, kNT, fb_smem<E>()));
+  *fb_blocks = std::min(b1, b2);
   return LB_OK;
 }
 
@@ -77,15 +101,19 @@ lb_status_t device_info(int dev, const DeviceInfo** out) {
   std::lock_guard<std::mutex> g(g_dev_mu);
   DeviceInfo& d = g_dev[dev];
   if (d.sm_count == 0) {
-    LB_CUDA(cudaDeviceGetAttribute(&d.sm_count, cudaDevAttrMultiProcessorCount, dev));
-    int b1 = 0, b2 = 0, b3 = 0, b4 = 0;
+    int sms = 0;
+    LB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int pb[kNumL], fb[kNumL];
     lb_status_t st;
-    if ((st = merge_prepare<1024, true>(&b1)) != LB_OK) return st;
-    if ((st = merge_prepare<1024, false>(&b2)) != LB_OK) return st;
-    if ((st = merge_prepare<2048, true>(&b3)) != LB_OK) return st;
-    if ((st = merge_prepare<2048, false>(&b4)) != LB_OK) return st;
-    d.grid_1024 = d.sm_count * std::max(1, std::min(b1, b2));
-    d.grid_2048 = d.sm_count * std::max(1, std::min(b3, b4));
+    if ((st = prepare_e<4>(&pb[0], &fb[0])) != LB_OK) return st;
+    if ((st = prepare_e<8>(&pb[1], &fb[1])) != LB_OK) return st;
+    if ((st = prepare_e<12>(&pb[2], &fb[2])) != LB_OK) return st;
+    if ((st = prepare_e<16>(&pb[3], &fb[3])) != LB_OK) return st;
+    for (int i = 0; i < kNumL; ++i) {
+      d.pipe_grid[i] = sms * std::max(1, pb[i]);
+      d.fb_grid[i] = sms * std::max(1, fb[i]);
+    }
+    d.sm_count = sms;
   }
   *out = &d;
   return LB_OK;
@@ -101,6 +129,7 @@ struct lb_csr_s {
   int device = 0;
   const DeviceInfo* dev = nullptr;
   bool vec = true;            // col/val 16-byte aligned -> 128-bit loads
+  bool pipe = true;           // off/col/val 16-byte aligned -> TMA-pipelined tile kernel
   int L = LB_DEFAULT_ITEMS_PER_TILE;
   bool coords_valid = false;
   bool owns_scratch = true;
@@ -108,6 +137,7 @@ struct lb_csr_s {
   int* carry_row = nullptr;   // [kMaxCtas]
   float* carry_val = nullptr; // [kMaxCtas]
   int* flags = nullptr;       // [4] validation flags
+  unsigned* ticket = nullptr; // [1] last-CTA ticket of the pipelined kernel (kept at 0 between launches)
 };
 
 namespace {
@@ -118,7 +148,7 @@ size_t align256(size_t n) { return (n + 255) & ~size_t(255); }
 
 size_t scratch_bytes(int64_t rows, int64_t nnz) {
   return align256((num_tiles(rows, nnz, kMinTile) + 1) * sizeof(int2)) + align256(kMaxCtas * sizeof(int)) +
-         align256(kMaxCtas * sizeof(float)) + align256(4 * sizeof(int));
+         align256(kMaxCtas * sizeof(float)) + align256(4 * sizeof(int)) + align256(sizeof(unsigned));
 }
 
 void carve_scratch(lb_csr_s* A, char* p) {
@@ -129,6 +159,8 @@ void carve_scratch(lb_csr_s* A, char* p) {
   A->carry_val = reinterpret_cast<float*>(p);
   p += align256(kMaxCtas * sizeof(float));
   A->flags = reinterpret_cast<int*>(p);
+  p += align256(4 * sizeof(int));
+  A->ticket = reinterpret_cast<unsigned*>(p);
 }
 
 lb_status_t check_shape(int64_t rows, int64_t cols, int64_t nnz) {
@@ -148,6 +180,7 @@ lb_status_t init_handle(lb_csr_s* A, int64_t rows, int64_t cols, int64_t nnz, co
   lb_status_t st = device_info(A->device, &A->dev);
   if (st != LB_OK) return st;
   A->vec = (reinterpret_cast<uintptr_t>(col) % 16 == 0) && (reinterpret_cast<uintptr_t>(val) % 16 == 0);
+  A->pipe = A->vec && (reinterpret_cast<uintptr_t>(off) % 16 == 0);
   return LB_OK;
 }
 
@@ -177,8 +210,14 @@ lb_status_t launch_partition(const lb_csr_s* A, int64_t L, int2* coords, stream_
   return LB_OK;
 }
 
-template <int L, bool VEC>
+// Phase hooks for lb_spmv_phase_times (events recorded between phases when non-null).
+struct PhaseEvents {
+  cudaEvent_t ev[4];
+};
+
+template <int E, bool VEC>
 lb_status_t launch_merge_tiles(lb_csr_s* A, const float* x, float* y, int grid_max, int* grid_used, stream_t s) {
+  constexpr int L = kNT * E - 8;
   const int T = (int)num_tiles(A->rows, A->nnz, L);
   int grid = std::min(T, std::min(grid_max, kMaxCtas));
   const int tpc = (T + grid - 1) / grid;
@@ -188,16 +227,59 @@ lb_status_t launch_merge_tiles(lb_csr_s* A, const float* x, float* y, int grid_m
   a.coords = A->coords; a.rows = (int)A->rows; a.nnz = (int)A->nnz;
   a.num_tiles = T; a.tiles_per_cta = tpc;
   a.carry_row = A->carry_row; a.carry_val = A->carry_val;
-  lbk::merge_tile_kernel<kNT, L, VEC><<<grid, kNT, merge_smem<L, VEC>(), s>>>(a);
+  lbk::merge_tile_kernel<kNT, L, VEC><<<grid, kNT, fb_smem<E>(), s>>>(a);
   LB_LAUNCHED();
   *grid_used = grid;
   return LB_OK;
 }
 
-// Phase hooks for lb_spmv_phase_times (events recorded between phases when non-null).
-struct PhaseEvents {
-  cudaEvent_t ev[4];
-};
+template <int E>
+lb_status_t launch_merge_pipe(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s) {
+  constexpr int L = kNT * E - 8;
+  const int T = (int)num_tiles(A->rows, A->nnz, L);
+  int grid = std::min(T, std::min(grid_max, kMaxCtas));
+  const int tpc = (T + grid - 1) / grid;
+  grid = (T + tpc - 1) / tpc;
+  lbk::PipeArgs a;
+  a.off = A->off; a.col = A->col; a.val = A->val; a.x = x; a.y = y;
+  a.coords = A->coords; a.rows = (int)A->rows; a.nnz = (int)A->nnz;
+  a.num_tiles = T; a.tiles_per_cta = tpc;
+  a.carry_row = A->carry_row; a.carry_val = A->carry_val; a.ticket = A->ticket;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kNT);
+  cfg.dynamicSmemBytes = pipe_smem<E>();
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL after lb_partition
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = getenv("LB_NO_PDL") ? 0 : 1;
+  LB_CUDA(cudaLaunchKernelEx(&cfg, lbk::merge_pipe_kernel<kNT, E, kPipeStages>, a));
+  LB_LAUNCHED();
+  return LB_OK;
+}
+
+template <int E>
+lb_status_t launch_merge(lb_csr_s* A, const float* x, float* y, stream_t s, PhaseEvents* pe) {
+  const int li = l_index(kNT * E - 8);
+  if (A->pipe) {
+    lb_status_t st = launch_merge_pipe<E>(A, x, y, A->dev->pipe_grid[li], s);
+    if (st != LB_OK) return st;
+    if (pe) { LB_CUDA(cudaEventRecord(pe->ev[2], s)); LB_CUDA(cudaEventRecord(pe->ev[3], s)); }
+    return LB_OK;
+  }
+  int grid = 0;
+  lb_status_t st = A->vec ? launch_merge_tiles<E, true>(A, x, y, A->dev->fb_grid[li], &grid, s)
+                          : launch_merge_tiles<E, false>(A, x, y, A->dev->fb_grid[li], &grid, s);
+  if (st != LB_OK) return st;
+  if (pe) LB_CUDA(cudaEventRecord(pe->ev[2], s));
+  lbk::fixup_kernel<<<(grid + kNT - 1) / kNT, kNT, 0, s>>>((int)A->rows, grid, A->carry_row, A->carry_val, y);
+  LB_LAUNCHED();
+  if (pe) LB_CUDA(cudaEventRecord(pe->ev[3], s));
+  return LB_OK;
+}
+
 
 lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y, uint32_t flags, stream_t s,
                       PhaseEvents* pe) {
@@ -238,19 +320,13 @@ lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y
         A->coords_valid = true;
       }
       if (pe) LB_CUDA(cudaEventRecord(pe->ev[1], s));
-      int grid = 0;
-      if (A->L == 1024)
-        st = A->vec ? launch_merge_tiles<1024, true>(A, x, y, A->dev->grid_1024, &grid, s)
-                    : launch_merge_tiles<1024, false>(A, x, y, A->dev->grid_1024, &grid, s);
-      else
-        st = A->vec ? launch_merge_tiles<2048, true>(A, x, y, A->dev->grid_2048, &grid, s)
-                    : launch_merge_tiles<2048, false>(A, x, y, A->dev->grid_2048, &grid, s);
-      if (st != LB_OK) return st;
-      if (pe) LB_CUDA(cudaEventRecord(pe->ev[2], s));
-      lbk::fixup_kernel<<<(grid + kNT - 1) / kNT, kNT, 0, s>>>((int)A->rows, grid, A->carry_row, A->carry_val, y);
-      LB_LAUNCHED();
-      if (pe) LB_CUDA(cudaEventRecord(pe->ev[3], s));
-      return LB_OK;
+      switch (A->L) {
+        case 1016: return launch_merge<4>(A, x, y, s, pe);
+        case 2040: return launch_merge<8>(A, x, y, s, pe);
+        case 3064: return launch_merge<12>(A, x, y, s, pe);
+        case 4088: return launch_merge<16>(A, x, y, s, pe);
+        default: return fail(LB_ERR_INVALID_ARG, "unsupported tile length %d", A->L);
+      }
     }
     default:
       return fail(LB_ERR_INVALID_ARG, "unknown schedule id %d", (int)sched);
@@ -284,6 +360,8 @@ lb_status_t lb_csr_create(int64_t rows, int64_t cols, int64_t nnz, const int32_t
   cudaError_t e = cudaMalloc(&p, scratch_bytes(rows, nnz));
   if (e != cudaSuccess) { delete A; return fail(LB_ERR_OOM, "cudaMalloc scratch: %s", cudaGetErrorString(e)); }
   carve_scratch(A, static_cast<char*>(p));
+  e = cudaMemsetAsync(A->ticket, 0, sizeof(unsigned), S(stream));
+  if (e != cudaSuccess) { cudaFree(p); delete A; return fail(LB_ERR_CUDA, "cudaMemsetAsync: %s", cudaGetErrorString(e)); }
   if (validate) {
     st = run_validate(A, S(stream));
     if (st != LB_OK) { cudaFree(p); delete A; return st; }
@@ -302,7 +380,7 @@ lb_status_t lb_csr_destroy(lb_csr_t A) {
 lb_status_t lb_csr_set_items_per_tile(lb_csr_t A, int32_t items_per_tile) {
   if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
   int L = items_per_tile == 0 ? LB_DEFAULT_ITEMS_PER_TILE : items_per_tile;
-  if (L != 1024 && L != 2048) return fail(LB_ERR_INVALID_ARG, "items_per_tile %d unsupported (1024, 2048)", L);
+  if (l_index(L) < 0) return fail(LB_ERR_INVALID_ARG, "items_per_tile %d unsupported (1016, 2040, 3064, 4088)", L);
   A->L = L;
   A->coords_valid = false;
   return LB_OK;
@@ -378,6 +456,7 @@ lb_status_t lb_spmv_host(int64_t rows, int64_t cols, int64_t nnz, const int32_t*
   A.owns_scratch = false;
   if ((st = init_handle(&A, rows, cols, nnz, d_off, d_col, d_val)) != LB_OK) return st;
   carve_scratch(&A, p);
+  LB_CUDA(cudaMemsetAsync(A.ticket, 0, sizeof(unsigned), s));
   LB_CUDA(cudaMemcpyAsync(d_off, h_row_offsets, (rows + 1) * 4, cudaMemcpyHostToDevice, s));
   if (nnz > 0) {
     LB_CUDA(cudaMemcpyAsync(d_col, h_col_idx, nnz * 4, cudaMemcpyHostToDevice, s));

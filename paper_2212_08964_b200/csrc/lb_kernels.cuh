@@ -84,6 +84,8 @@ __global__ void validate_kernel(int rows, int cols, int nnz, const int* __restri
 // [max(0, d-nnz), min(d, rows)] (below d-nnz every row end precedes d).
 __global__ void partition_kernel(int rows, int nnz, const int* __restrict__ off, int64_t L, int64_t T,
                                  int2* __restrict__ coords) {
+  // PDL: let the dependent tile kernel start its prologue now (it waits for our completion)
+  asm volatile("griddepcontrol.launch_dependents;");
   int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t > T) return;
   const int64_t total = (int64_t)rows + nnz;
@@ -121,7 +123,6 @@ struct MergeCfg {
   static constexpr int kChunks = kNV * kWarps;              // 128-nonzero chunks per tile
   static constexpr int kTailWords = (4 * kSlots + 31) / 32;
   static_assert(kChunks <= 32, "chunk scan uses one warp");
-  static_assert(L % NT == 0, "tile length must be a multiple of the CTA width");
   struct Smem {
     unsigned tail[2][kTailWords];  // bit q set: local nonzero q (from j0&~3) ends its row
     int rowend[2][L];              // local end (exclusive) of each row ending in the tile
@@ -136,7 +137,7 @@ template <int NT, int L, bool VEC>
 __global__ void __launch_bounds__(NT, 3) merge_tile_kernel(MergeArgs a) {
   using Cfg = MergeCfg<NT, L, VEC>;
   constexpr int NV = Cfg::kNV;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   typename Cfg::Smem& sm = *reinterpret_cast<typename Cfg::Smem*>(smem_raw);
 
   const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -297,6 +298,278 @@ __global__ void fixup_kernel(int rows, int n, const int* __restrict__ carry_row,
   float s = 0.f;
   for (int k = c; k < n && carry_row[k] == r; ++k) s += carry_val[k];
   y[r] += s;
+}
+
+// ----------------------------------------------------------------------------- merge-path tiles, TMA pipeline
+// sm_100a tile processor used when row_offsets / col_idx / values are 16-byte aligned:
+//  * one elected thread streams each upcoming tile's col/val/offset ranges into an S-stage
+//    shared-memory ring with cp.async.bulk (TMA bulk copies, L2 evict-first), completing on an
+//    mbarrier per stage, so DRAM latency is off the critical path;
+//  * the row pass writes, for every nonzero that ends a row, the row's local index
+//    (tailrow[q] = r + 1) -- no atomics -- and writes y = 0 (+carry) for rows with no nonzero in
+//    the tile;
+//  * the nonzero pass reads col/val/tailrow with 128/64-bit shared loads, gathers x, runs the
+//    warp segmented scan + chunk scan, and the thread owning a row's last nonzero stores y[row];
+//  * two __syncthreads per tile; the fix-up (Alg.3) runs in the last CTA to finish
+//    (atomic ticket), in CTA order (deterministic).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+// Wait for the phase with parity `parity` to complete.  Watchdog: a stage must land within
+// milliseconds; after ~2^32 cycles the kernel traps (an error, never a silent hang).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  const long long t0 = clock64();
+  for (;;) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_addr(bar)), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (clock64() - t0 > (1ll << 32)) __trap();  // ~2 s at 2 GHz
+  }
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// global -> shared bulk copy (16-byte aligned, size multiple of 16), completes on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+
+struct PipeArgs {
+  const int* off;
+  const int* col;
+  const float* val;
+  const float* x;
+  float* y;
+  const int2* coords;
+  int rows, nnz;
+  int num_tiles;
+  int tiles_per_cta;
+  int* carry_row;
+  float* carry_val;
+  unsigned* ticket;  // zero before launch; the last CTA resets it
+};
+
+// Tile length for E nonzeros per thread: the 16-byte-aligned nonzero range of a tile spans at
+// most L + 6 elements, so L = NT*E - 8 fills every thread (tile quantisation).
+template <int NT, int E>
+constexpr int pipe_tile_len() { return NT * E - 8; }
+
+template <int NT, int E, int S>
+struct PipeCfg {
+  static constexpr int L = pipe_tile_len<NT, E>();
+  static constexpr int kCap = NT * E;                // staged elements per array per stage (>= L + 8)
+  static constexpr int kWarps = NT / 32;
+  static_assert(E % 4 == 0 && E >= 4 && E <= 16, "E: multiple of 4 in [4, 16]");
+  static_assert(kWarps <= 32, "chunk scan uses one warp");
+  struct Smem {
+    int col[S][kCap];
+    float val[S][kCap];
+    int off[S][kCap];
+    unsigned short tailrow[2][kCap];  // local row index + 1 of the row ending at nonzero q (0: none)
+    uint64_t bar[S];
+    int cflag[kWarps];
+    float cval[kWarps];
+    int last;
+  };
+};
+
+template <int NT, int E, int S>
+__device__ __forceinline__ void pipe_issue(const PipeArgs& a, typename PipeCfg<NT, E, S>::Smem& sm, int t, int stage,
+                                           uint64_t pol) {
+  // called by one thread: stage tile t's offsets [i0&~3, i1], col/val [j0&~3, j1)
+  const int2 c0 = a.coords[t], c1 = a.coords[t + 1];
+  const int oA = c0.x & ~3, oEnd = c1.x + 1;           // need off[i0 .. i1]
+  const int jA = c0.y & ~3, jEnd = c1.y;
+  const int oLim = (a.rows + 1) & ~3, jLim = a.nnz & ~3; // bulk copies stay inside the arrays
+  const int oB = max(oA, min((oEnd + 3) & ~3, oLim));
+  const int jB = max(jA, min((jEnd + 3) & ~3, jLim));
+  const uint32_t ob = 4u * (oB - oA), jb = 4u * (jB - jA);
+  mbar_arrive_expect_tx(&sm.bar[stage], ob + 2 * jb);
+  if (ob) bulk_g2s(&sm.off[stage][0], a.off + oA, ob, &sm.bar[stage], pol);
+  if (jb) {
+    bulk_g2s(&sm.col[stage][0], a.col + jA, jb, &sm.bar[stage], pol);
+    bulk_g2s(&sm.val[stage][0], a.val + jA, jb, &sm.bar[stage], pol);
+  }
+  // array-end remainders (< 4 elements): generic stores, published by a later __syncthreads
+  for (int k = oB; k < oEnd; ++k) sm.off[stage][k - oA] = __ldg(a.off + k);
+  for (int k = jB; k < jEnd; ++k) {
+    sm.col[stage][k - jA] = __ldg(a.col + k);
+    sm.val[stage][k - jA] = __ldg(a.val + k);
+  }
+}
+
+template <int NT, int E, int S>
+__global__ void __launch_bounds__(NT, 2) merge_pipe_kernel(PipeArgs a) {
+  using Cfg = PipeCfg<NT, E, S>;
+  constexpr int kW = Cfg::kWarps;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  typename Cfg::Smem& sm = *reinterpret_cast<typename Cfg::Smem*>(smem_raw);
+
+  const unsigned tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t_begin = blockIdx.x * a.tiles_per_cta;
+  const int t_end = min(a.num_tiles, t_begin + a.tiles_per_cta);
+  const uint64_t pol = policy_evict_first();
+  const int q_begin = E * (int)tid;  // this thread's contiguous local nonzero positions [q_begin, q_begin+E)
+
+  for (int w = tid; w < 2 * Cfg::kCap; w += NT) (&sm.tailrow[0][0])[w] = 0;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&sm.bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  // PDL: everything above overlapped the partition kernel; coords are read below.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (tid == 0)
+    for (int s = 0; s < S && t_begin + s < t_end; ++s) pipe_issue<NT, E, S>(a, sm, t_begin + s, s, pol);
+  __syncthreads();  // publishes the prologue's generic (array-end) stores
+
+  float cta_carry = 0.f;
+  int i_last = 0;
+  for (int t = t_begin; t < t_end; ++t) {
+    const int n = t - t_begin;
+    const int st = n % S;
+    const int b = n & 1;
+    const int2 c0 = a.coords[t], c1 = a.coords[t + 1];
+    const int i0 = c0.x, j0 = c0.y, i1 = c1.x, j1 = c1.y;
+    const int nrows = i1 - i0;
+    const int jA = j0 & ~3, oA = i0 & ~3;
+    const int lo = j0 - jA, hi = j1 - jA;
+    mbar_wait(&sm.bar[st], (uint32_t)((n / S) & 1));
+
+    // (1) row pass: mark each row's last nonzero in the tile, or write rows without one
+    {
+      const int* so = &sm.off[st][i0 - oA];
+      for (int r = tid; r < nrows; r += NT) {
+        const int e = so[r + 1] - jA;
+        const int s = r == 0 ? lo : so[r] - jA;
+        if (e > s) sm.tailrow[b][e - 1] = (unsigned short)(r + 1);
+        else a.y[i0 + r] = r == 0 ? cta_carry : 0.f;
+      }
+    }
+    __syncthreads();
+
+    // (2) nonzero pass over this thread's E contiguous positions
+    float first_val = 0.f, run = 0.f;
+    int first_r = -1;
+    unsigned tmask = 0u;
+    if (q_begin < hi) {
+      int cc[E];
+      float vv[E], xv[E];
+      unsigned tr[E / 2];
+#pragma unroll
+      for (int k = 0; k < E / 4; ++k) {
+        const int4 ci = *reinterpret_cast<const int4*>(&sm.col[st][q_begin + 4 * k]);
+        const float4 vi = *reinterpret_cast<const float4*>(&sm.val[st][q_begin + 4 * k]);
+        const uint2 ti = *reinterpret_cast<const uint2*>(&sm.tailrow[b][q_begin + 4 * k]);
+        cc[4 * k] = ci.x; cc[4 * k + 1] = ci.y; cc[4 * k + 2] = ci.z; cc[4 * k + 3] = ci.w;
+        vv[4 * k] = vi.x; vv[4 * k + 1] = vi.y; vv[4 * k + 2] = vi.z; vv[4 * k + 3] = vi.w;
+        tr[2 * k] = ti.x; tr[2 * k + 1] = ti.y;
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {  // all gathers in flight before any use
+        const bool ok = q_begin + e >= lo && q_begin + e < hi;
+        xv[e] = ok ? ld_x(a.x + cc[e]) : 0.f;
+        if (!ok) vv[e] = 0.f;
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        run = fmaf(vv[e], xv[e], run);
+        const unsigned rid = (e & 1) ? (tr[e >> 1] >> 16) : (tr[e >> 1] & 0xFFFFu);
+        if (rid) {
+          const int r = (int)rid - 1;
+          if (first_r < 0) {
+            first_r = r;          // needs the carry-in from earlier threads: stored after the scans
+            first_val = run;
+          } else {
+            a.y[i0 + r] = run;    // row started in this thread: final (r > 0 here)
+          }
+          run = 0.f;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < E / 2; ++k) tmask |= tr[k];
+    }
+    bool f = first_r >= 0;
+    float val = run;
+    warp_segscan_incl(f, val, lane);
+    float lval = __shfl_up_sync(kFull, val, 1);      // every lane must execute full-mask shuffles
+    const int lf = __shfl_up_sync(kFull, (int)f, 1);
+    const bool lflag = lane ? (bool)lf : false;
+    if (lane == 0) lval = 0.f;
+    if (lane == 31) {
+      sm.cflag[warp] = f;
+      sm.cval[warp] = val;
+    }
+    __syncthreads();
+    // stage st is fully consumed: refill it with tile t + S (async proxy after generic reads)
+    if (tid == 0 && t + S < t_end) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      pipe_issue<NT, E, S>(a, sm, t + S, st, pol);
+    }
+
+    // (3) warp-chunk scan; the first row end of each thread gets its carry-in
+    bool cf = lane < (unsigned)kW ? (bool)sm.cflag[lane] : false;
+    float cv = lane < (unsigned)kW ? sm.cval[lane] : 0.f;
+    warp_segscan_incl(cf, cv, lane);
+    const float agg_val = __shfl_sync(kFull, cv, kW - 1);
+    float ex_v = __shfl_up_sync(kFull, cv, 1);
+    if (lane == 0) ex_v = 0.f;
+    const float chunk_in = __shfl_sync(kFull, ex_v, warp);
+    if (first_r >= 0) {
+      float yv = (lflag ? lval : chunk_in + lval) + first_val;
+      if (first_r == 0) yv += cta_carry;
+      a.y[i0 + first_r] = yv;
+    }
+    if (tmask) {  // clear this thread's row marks for tile t+2
+#pragma unroll
+      for (int k = 0; k < E / 4; ++k) *reinterpret_cast<uint2*>(&sm.tailrow[b][q_begin + 4 * k]) = make_uint2(0u, 0u);
+    }
+    cta_carry = nrows > 0 ? agg_val : cta_carry + agg_val;
+    i_last = i1;
+  }
+
+  // carry of this CTA's run, then the last CTA to finish applies all carries (Alg.3 fix-up)
+  if (tid == 0) {
+    if (t_begin < t_end) {
+      a.carry_row[blockIdx.x] = i_last;
+      a.carry_val[blockIdx.x] = cta_carry;
+    }
+    __threadfence();
+    const unsigned done = atomicAdd(a.ticket, 1u);
+    sm.last = done == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (sm.last) {
+    __threadfence();
+    const int nc = (int)gridDim.x;
+    for (int c = tid; c < nc; c += NT) {
+      const int r = __ldcg(a.carry_row + c);
+      if (r >= a.rows) continue;
+      if (c > 0 && __ldcg(a.carry_row + c - 1) == r) continue;
+      float s = 0.f;
+      for (int k = c; k < nc && __ldcg(a.carry_row + k) == r; ++k) s += __ldcg(a.carry_val + k);
+      a.y[r] = __ldcg(a.y + r) + s;
+    }
+    if (tid == 0) *a.ticket = 0u;
+  }
 }
 
 // ----------------------------------------------------------------------------- thread-mapped

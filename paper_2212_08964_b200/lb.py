@@ -15,13 +15,14 @@ import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_PKG)
-LIB_PATH = os.path.join(_PKG, "liblb.so")
+LIB_PATH = os.environ.get("LB_LIB_PATH") or os.path.join(_PKG, "liblb.so")
 HEADER = os.path.join(_ROOT, "include", "lb.h")
 
 LB_OK, LB_ERR_INVALID_ARG, LB_ERR_INVALID_CSR, LB_ERR_UNSUPPORTED, LB_ERR_OOM, LB_ERR_CUDA, LB_ERR_NCCL = range(7)
 SCHEDULES = {"thread_mapped": 0, "group_mapped": 1, "merge_path": 2, "block_mapped": 3}
 LB_SPMV_REPARTITION = 1
-DEFAULT_ITEMS_PER_TILE = 2048
+DEFAULT_ITEMS_PER_TILE = 1016
+TILE_LENGTHS = (1016, 2040, 3064, 4088)
 
 
 class LbError(RuntimeError):

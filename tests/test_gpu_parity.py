@@ -75,7 +75,7 @@ SMALL = {
 
 # ---------------------------------------------------------------- partition (bit-exact)
 
-@pytest.mark.parametrize("L", [1, 2, 3, 7, 256, 1024, 2048, 5000])
+@pytest.mark.parametrize("L", [1, 2, 3, 7, 256, 1016, 2048, 3064, 5000])
 @pytest.mark.parametrize("name", ["rmat12", "stencil100", "skewed", "c1"])
 def test_partition_bit_exact(name, L):
     A = SMALL[name]("int")
@@ -114,7 +114,7 @@ def test_spmv_tolerance(name, sched):
     check_y(run(A, x, sched), y_ref, s_ref, False, f"{name}/{sched}")
 
 
-@pytest.mark.parametrize("L", [1024, 2048])
+@pytest.mark.parametrize("L", [1016, 2040, 3064, 4088])
 @pytest.mark.parametrize("vmode", ["int", "float"])
 def test_merge_path_tile_lengths(L, vmode):
     A = lbgen.rmat(13, 16, 5, vmode)
@@ -242,6 +242,8 @@ def test_argument_errors():
         M.spmv(x, schedule=17)
     with pytest.raises(lb.LbError):
         M.set_items_per_tile(3000)
+    with pytest.raises(lb.LbError):
+        M.set_items_per_tile(2048)
     with pytest.raises(ValueError):
         M.spmv(torch.ones(A.cols + 1, device="cuda"))
 
@@ -263,7 +265,7 @@ def test_launch_count_and_phase_times():
     y = torch.empty(A.rows, device="cuda")
     n0 = lb.launch_count()
     M.spmv(x, y, "merge_path", repartition=True)
-    assert lb.launch_count() - n0 == 3          # partition + tiles + fix-up
+    assert lb.launch_count() - n0 in (2, 3)     # partition + tiles (+ fix-up kernel on the unaligned path)
     ms = M.phase_times(x, y, "merge_path")
     assert len(ms) == 3 and all(v >= 0 for v in ms) and ms[1] > 0
 
@@ -349,7 +351,7 @@ def test_full_size_configs(cfg):
         M = lb.CsrMatrix.from_csr(A, device="cuda")
         if vmode == "int":
             coords = M.partition().cpu().numpy()
-            assert np.array_equal(coords, oracle.partition(A.row_offsets.cpu(), 2048)), "partition"
+            assert np.array_equal(coords, oracle.partition(A.row_offsets.cpu(), M.items_per_tile)), "partition"
         else:
             coords = M.partition().cpu().numpy()
         full = vmode == "int" and cfg != "c5"

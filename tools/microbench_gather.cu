@@ -129,14 +129,14 @@ int main() {
     printf("copy_f4   grid=%d*%d: %.3f ms  %.1f GB/s (r+w)\n", sms, bpsm, ms, N * 8 / ms / 1e6);
   }
   const size_t G = 1ull << 28;  // gathers per launch
-  for (uint32_t logm : {20u, 24u, 26u, 28u}) {
+  for (uint32_t logm : {10u, 12u, 14u, 15u, 16u, 20u, 24u}) {
     uint32_t mask = (1u << logm) - 1;
     float t0 = time_ms([&] { k_gather_hash<0, 8><<<sms * 8, 256>>>(a, mask, G, out); });
     float t1 = time_ms([&] { k_gather_hash<1, 8><<<sms * 8, 256>>>(a, mask, G, out); });
     float t2 = time_ms([&] { k_gather_hash<2, 8><<<sms * 8, 256>>>(a, mask, G, out); });
     float t3 = time_ms([&] { k_gather_hash<3, 8><<<sms * 8, 256>>>(a, mask, G, out); });
     float t4 = time_ms([&] { k_gather_hash<4, 8><<<sms * 8, 256>>>(a, mask, G, out); });
-    printf("gather_hash x=%4u MB: G/s default %.1f  ldg %.1f  na %.1f  cg %.1f  evl %.1f\n", (1u << logm) * 4 >> 20,
+    printf("gather_hash x=%8u KB: G/s default %.1f  ldg %.1f  na %.1f  cg %.1f  evl %.1f\n", (1u << logm) * 4 >> 10,
            G / t0 / 1e6, G / t1 / 1e6, G / t2 / 1e6, G / t3 / 1e6, G / t4 / 1e6);
   }
   int* col; CK(cudaMalloc(&col, G * 4));
