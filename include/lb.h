@@ -77,8 +77,8 @@ typedef struct lb_csr_s* lb_csr_t;   /* opaque CSR handle (borrowed arrays + own
 typedef struct lb_comm_s* lb_comm_t; /* opaque multi-GPU communicator (wraps an ncclComm_t) */
 
 /* Default merge-path tile length L (merge items per tile) used by lb_spmv.  Supported lengths are
- * L = 256*E - 8 for E = 4, 8, 12, 16 nonzeros per thread: a tile's 16-byte-aligned nonzero range
- * spans at most L + 6 elements, so every one of the 256 threads of the CTA gets E of them. */
+ * L = NT*E - 8 for NT threads x E nonzeros per thread (E a multiple of 4): a tile's 16-byte-aligned range
+ * of nonzeros spans at most L + 6 elements, so every thread of the CTA gets E of them. */
 #define LB_DEFAULT_ITEMS_PER_TILE 1016
 
 /*
@@ -102,7 +102,7 @@ lb_status_t lb_csr_destroy(lb_csr_t A);
 
 /*
  * lb_csr_set_items_per_tile -- choose the merge-path tile length L used by lb_spmv
- * (0 = LB_DEFAULT_ITEMS_PER_TILE).  Supported: 1016, 2040, 3064, 4088; anything else returns
+ * (0 = LB_DEFAULT_ITEMS_PER_TILE).  Supported: 504, 1016, 2040, 3064, 4088; anything else returns
  * LB_ERR_INVALID_ARG.
  * Invalidates the cached partition.  Not thread-safe with respect to in-flight lb_spmv.
  */

@@ -49,50 +49,122 @@ lb_status_t fail(lb_status_t st, const char* fmt, ...) {
 
 constexpr int kNT = 256;
 constexpr int kMaxCtas = 8192;      // carry slots per handle (>= SMs x resident CTAs)
-constexpr int kMinTile = 1016;      // smallest supported L: sizes the partition cache
+constexpr int kMinTile = 504;       // smallest supported L: sizes the partition cache
 
-// Merge-path tile lengths: L = 256*E - 8 for E nonzeros per thread (see PipeCfg).
-constexpr int kNumL = 4;
-constexpr int kE[kNumL] = {4, 8, 12, 16};
+// Merge-path tile lengths.  The pipelined kernel runs NT threads x E nonzeros per tile, so a
+// tile holds L = NT*E - 8 merge items (its 16-byte-aligned nonzero range spans <= L + 6).
+constexpr int kNumL = 5;
+constexpr int kTileL[kNumL] = {504, 1016, 2040, 3064, 4088};
 constexpr int kPipeStages = 2;
-inline int l_of(int e) { return kNT * e - 8; }
 inline int l_index(int L) {
   for (int i = 0; i < kNumL; ++i)
-    if (l_of(kE[i]) == L) return i;
+    if (kTileL[i] == L) return i;
   return -1;
 }
 
+using stream_t = cudaStream_t;
+inline stream_t S(void* s) { return reinterpret_cast<stream_t>(s); }
+
+typedef lb_status_t (*pipe_launch_fn)(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s);
+typedef lb_status_t (*pipe_prepare_fn)(int* blocks_per_sm);
+
+// One configuration of a merge-path tile kernel (kind 0: direct, kind 1: TMA-staged).
+struct PipeVariant {
+  int L, nt, e, minb, kind;
+  pipe_prepare_fn prepare;
+  pipe_launch_fn launch;
+};
+
+template <int NT, int E, int MINB>
+size_t pipe_smem() { return sizeof(typename lbk::PipeCfg<NT, E, kPipeStages>::Smem); }
+
+template <int NT, int E, int MINB>
+lb_status_t pipe_prepare(int* blocks) {
+  auto k = lbk::merge_pipe_kernel<NT, E, kPipeStages, MINB>;
+  LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem<NT, E, MINB>()));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k, NT, pipe_smem<NT, E, MINB>()));
+  return LB_OK;
+}
+
+template <int NT, int E, int MINB>
+lb_status_t pipe_launch(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s);
+
+// Direct kernel: static smem only; after the occupancy query, ask for the smallest shared-memory
+// carve-out that still fits that occupancy, leaving the rest of the 256 KB to L1 (gather MLP).
+template <int NT, int MINB, bool XK>
+lb_status_t direct_prepare(int* blocks) {
+  auto k = lbk::merge_direct_kernel<NT, MINB, XK>;
+  cudaFuncAttributes fa;
+  LB_CUDA(cudaFuncGetAttributes(&fa, k));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k, NT, 0));
+  const double need = (double)(*blocks) * (fa.sharedSizeBytes + 1024);
+  int pct = (int)(100.0 * need / (228.0 * 1024.0)) + 1;
+  pct = std::min(100, std::max(1, pct));
+  LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k, NT, 0));
+  return LB_OK;
+}
+
+template <int NT, int MINB, bool XK>
+lb_status_t direct_launch(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s);
+
+template <int NT, int E, int MINB>
+lb_status_t wide_prepare(int* blocks) {
+  auto k = lbk::merge_wide_kernel<NT, E, MINB>;
+  cudaFuncAttributes fa;
+  LB_CUDA(cudaFuncGetAttributes(&fa, k));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k, NT, 0));
+  const double need = (double)(*blocks) * (fa.sharedSizeBytes + 1024);
+  int pct = (int)(100.0 * need / (228.0 * 1024.0)) + 1;
+  pct = std::min(100, std::max(1, pct));
+  LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k, NT, 0));
+  return LB_OK;
+}
+template <int NT, int E, int MINB>
+lb_status_t wide_launch(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s);
+#define LB_WIDE_VARIANT(NT, E, MINB) {NT * E - 8, NT, E, MINB, 2, wide_prepare<NT, E, MINB>, wide_launch<NT, E, MINB>}
+
+#define LB_DIRECT_VARIANT(NT, MINB, XK) \
+  {NT * 4 - 8, NT, 4, MINB, 0, direct_prepare<NT, MINB, XK>, direct_launch<NT, MINB, XK>}
+#define LB_PIPE_VARIANT(NT, E, MINB) {NT * E - 8, NT, E, MINB, 1, pipe_prepare<NT, E, MINB>, pipe_launch<NT, E, MINB>}
+const PipeVariant kVariants[] = {
+    LB_WIDE_VARIANT(128, 8, 8),        // 0 L=1016  default (C3 R-MAT, C4 skewed: best measured)
+    LB_WIDE_VARIANT(256, 8, 4),        // 1 L=2040  default (C2 stencil: best measured)
+    LB_WIDE_VARIANT(256, 16, 2),       // 2 L=4088  default
+    LB_DIRECT_VARIANT(128, 8, false),  // 3 L=504   default
+    LB_PIPE_VARIANT(256, 12, 2),       // 4 L=3064  default (TMA-staged)
+    LB_PIPE_VARIANT(256, 4, 2),        // 5 L=1016  alternative: TMA bulk-copy staging of col/val/off
+    LB_DIRECT_VARIANT(256, 2, false),  // 6 L=1016  alternative: 128-bit loads, 4 nonzeros per thread
+    LB_WIDE_VARIANT(64, 8, 16),        // 7 L=504   alternative
+    LB_DIRECT_VARIANT(128, 4, true),   // 8 L=504   alternative: x gathers with L2 evict_last
+};
+constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
+// default variant per tile length (index into kVariants), chosen by measurement
+constexpr int kDefaultVariant[kNumL] = {3, 0, 1, 4, 2};  // per kTileL entry
+
 struct DeviceInfo {
   int sm_count = 0;
-  int fb_grid[kNumL] = {0};    // persistent grid of the fallback (unaligned) merge kernel per L
-  int pipe_grid[kNumL] = {0};  // persistent grid of the TMA-pipelined merge kernel per L
+  int fb_grid[kNumL] = {0};              // persistent grid of the fallback (unaligned) merge kernel per L
+  int pipe_grid[kNumVariants] = {0};     // persistent grid of each pipelined variant
 };
 
 DeviceInfo g_dev[64];
 std::mutex g_dev_mu;
 
-using stream_t = cudaStream_t;
-inline stream_t S(void* s) { return reinterpret_cast<stream_t>(s); }
+template <int L>
+size_t fb_smem() { return sizeof(typename lbk::MergeCfg<kNT, L, true>::Smem); }
 
-template <int E>
-size_t pipe_smem() { return sizeof(typename lbk::PipeCfg<kNT, E, kPipeStages>::Smem); }
-template <int E>
-size_t fb_smem() { return sizeof(typename lbk::MergeCfg<kNT, kNT * E - 8, true>::Smem); }
-
-template <int E>
-lb_status_t prepare_e(int* pipe_blocks, int* fb_blocks) {
-  auto kp = lbk::merge_pipe_kernel<kNT, E, kPipeStages>;
-  LB_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pipe_smem<E>()));
-  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(pipe_blocks, kp, kNT, pipe_smem<E>()));
-  constexpr int L = kNT * E - 8;
+template <int L>
+lb_status_t fb_prepare(int* blocks) {
   auto k1 = lbk::merge_tile_kernel<kNT, L, true>;
   auto k2 = lbk::merge_tile_kernel<kNT, L, false>;
   int b1 = 0, b2 = 0;
-  LB_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb_smem<E>()));
-  LB_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb_smem<E>()));
-  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k1, kNT, fb_smem<E>()));
-  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2, kNT, fb_smem<E>()));
-  *fb_blocks = std::min(b1, b2);
+  LB_CUDA(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb_smem<L>()));
+  LB_CUDA(cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fb_smem<L>()));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k1, kNT, fb_smem<L>()));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k2, kNT, fb_smem<L>()));
+  *blocks = std::min(b1, b2);
   return LB_OK;
 }
 
@@ -103,20 +175,34 @@ lb_status_t device_info(int dev, const DeviceInfo** out) {
   if (d.sm_count == 0) {
     int sms = 0;
     LB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    int pb[kNumL], fb[kNumL];
+    int fb[kNumL];
     lb_status_t st;
-    if ((st = prepare_e<4>(&pb[0], &fb[0])) != LB_OK) return st;
-    if ((st = prepare_e<8>(&pb[1], &fb[1])) != LB_OK) return st;
-    if ((st = prepare_e<12>(&pb[2], &fb[2])) != LB_OK) return st;
-    if ((st = prepare_e<16>(&pb[3], &fb[3])) != LB_OK) return st;
-    for (int i = 0; i < kNumL; ++i) {
-      d.pipe_grid[i] = sms * std::max(1, pb[i]);
-      d.fb_grid[i] = sms * std::max(1, fb[i]);
+    if ((st = fb_prepare<504>(&fb[0])) != LB_OK) return st;
+    if ((st = fb_prepare<1016>(&fb[1])) != LB_OK) return st;
+    if ((st = fb_prepare<2040>(&fb[2])) != LB_OK) return st;
+    if ((st = fb_prepare<3064>(&fb[3])) != LB_OK) return st;
+    if ((st = fb_prepare<4088>(&fb[4])) != LB_OK) return st;
+    for (int i = 0; i < kNumL; ++i) d.fb_grid[i] = sms * std::max(1, fb[i]);
+    for (int v = 0; v < kNumVariants; ++v) {
+      int b = 0;
+      if ((st = kVariants[v].prepare(&b)) != LB_OK) return st;
+      d.pipe_grid[v] = sms * std::max(1, b);
     }
     d.sm_count = sms;
   }
   *out = &d;
   return LB_OK;
+}
+
+// Development override: LB_PIPE_VARIANT=<index> forces a pipelined variant (its L must match).
+int pipe_variant_for(int L) {
+  const int li = l_index(L);
+  const char* env = getenv("LB_PIPE_VARIANT");
+  if (env) {
+    const int v = atoi(env);
+    if (v >= 0 && v < kNumVariants && kVariants[v].L == L) return v;
+  }
+  return kDefaultVariant[li];
 }
 
 }  // namespace
@@ -130,6 +216,7 @@ struct lb_csr_s {
   const DeviceInfo* dev = nullptr;
   bool vec = true;            // col/val 16-byte aligned -> 128-bit loads
   bool pipe = true;           // off/col/val 16-byte aligned -> TMA-pipelined tile kernel
+  bool vec32 = true;          // col/val 32-byte aligned -> 256-bit loads (wide tile kernel)
   int L = LB_DEFAULT_ITEMS_PER_TILE;
   bool coords_valid = false;
   bool owns_scratch = true;
@@ -181,6 +268,7 @@ lb_status_t init_handle(lb_csr_s* A, int64_t rows, int64_t cols, int64_t nnz, co
   if (st != LB_OK) return st;
   A->vec = (reinterpret_cast<uintptr_t>(col) % 16 == 0) && (reinterpret_cast<uintptr_t>(val) % 16 == 0);
   A->pipe = A->vec && (reinterpret_cast<uintptr_t>(off) % 16 == 0);
+  A->vec32 = (reinterpret_cast<uintptr_t>(col) % 32 == 0) && (reinterpret_cast<uintptr_t>(val) % 32 == 0);
   return LB_OK;
 }
 
@@ -215,9 +303,8 @@ struct PhaseEvents {
   cudaEvent_t ev[4];
 };
 
-template <int E, bool VEC>
+template <int L, bool VEC>
 lb_status_t launch_merge_tiles(lb_csr_s* A, const float* x, float* y, int grid_max, int* grid_used, stream_t s) {
-  constexpr int L = kNT * E - 8;
   const int T = (int)num_tiles(A->rows, A->nnz, L);
   int grid = std::min(T, std::min(grid_max, kMaxCtas));
   const int tpc = (T + grid - 1) / grid;
@@ -227,15 +314,15 @@ lb_status_t launch_merge_tiles(lb_csr_s* A, const float* x, float* y, int grid_m
   a.coords = A->coords; a.rows = (int)A->rows; a.nnz = (int)A->nnz;
   a.num_tiles = T; a.tiles_per_cta = tpc;
   a.carry_row = A->carry_row; a.carry_val = A->carry_val;
-  lbk::merge_tile_kernel<kNT, L, VEC><<<grid, kNT, fb_smem<E>(), s>>>(a);
+  lbk::merge_tile_kernel<kNT, L, VEC><<<grid, kNT, fb_smem<L>(), s>>>(a);
   LB_LAUNCHED();
   *grid_used = grid;
   return LB_OK;
 }
 
-template <int E>
-lb_status_t launch_merge_pipe(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s) {
-  constexpr int L = kNT * E - 8;
+template <int NT, int E, int MINB>
+lb_status_t pipe_launch(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s) {
+  constexpr int L = NT * E - 8;
   const int T = (int)num_tiles(A->rows, A->nnz, L);
   int grid = std::min(T, std::min(grid_max, kMaxCtas));
   const int tpc = (T + grid - 1) / grid;
@@ -247,31 +334,87 @@ lb_status_t launch_merge_pipe(lb_csr_s* A, const float* x, float* y, int grid_ma
   a.carry_row = A->carry_row; a.carry_val = A->carry_val; a.ticket = A->ticket;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kNT);
-  cfg.dynamicSmemBytes = pipe_smem<E>();
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = pipe_smem<NT, E, MINB>();
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL after lb_partition
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = getenv("LB_NO_PDL") ? 0 : 1;
-  LB_CUDA(cudaLaunchKernelEx(&cfg, lbk::merge_pipe_kernel<kNT, E, kPipeStages>, a));
+  cfg.numAttrs = 1;
+  LB_CUDA(cudaLaunchKernelEx(&cfg, lbk::merge_pipe_kernel<NT, E, kPipeStages, MINB>, a));
   LB_LAUNCHED();
   return LB_OK;
 }
 
-template <int E>
+template <int NT, int MINB, bool XK>
+lb_status_t direct_launch(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s) {
+  constexpr int L = NT * 4 - 8;
+  const int T = (int)num_tiles(A->rows, A->nnz, L);
+  int grid = std::min(T, std::min(grid_max, kMaxCtas));
+  const int tpc = (T + grid - 1) / grid;
+  grid = (T + tpc - 1) / tpc;
+  lbk::PipeArgs a;
+  a.off = A->off; a.col = A->col; a.val = A->val; a.x = x; a.y = y;
+  a.coords = A->coords; a.rows = (int)A->rows; a.nnz = (int)A->nnz;
+  a.num_tiles = T; a.tiles_per_cta = tpc;
+  a.carry_row = A->carry_row; a.carry_val = A->carry_val; a.ticket = A->ticket;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL after lb_partition
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LB_CUDA(cudaLaunchKernelEx(&cfg, lbk::merge_direct_kernel<NT, MINB, XK>, a));
+  LB_LAUNCHED();
+  return LB_OK;
+}
+
+template <int NT, int E, int MINB>
+lb_status_t wide_launch(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s) {
+  constexpr int L = NT * E - 8;
+  const int T = (int)num_tiles(A->rows, A->nnz, L);
+  int grid = std::min(T, std::min(grid_max, kMaxCtas));
+  const int tpc = (T + grid - 1) / grid;
+  grid = (T + tpc - 1) / tpc;
+  lbk::PipeArgs a;
+  a.off = A->off; a.col = A->col; a.val = A->val; a.x = x; a.y = y;
+  a.coords = A->coords; a.rows = (int)A->rows; a.nnz = (int)A->nnz;
+  a.num_tiles = T; a.tiles_per_cta = tpc;
+  a.carry_row = A->carry_row; a.carry_val = A->carry_val; a.ticket = A->ticket;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL after lb_partition
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LB_CUDA(cudaLaunchKernelEx(&cfg, lbk::merge_wide_kernel<NT, E, MINB>, a));
+  LB_LAUNCHED();
+  return LB_OK;
+}
+
+template <int L>
 lb_status_t launch_merge(lb_csr_s* A, const float* x, float* y, stream_t s, PhaseEvents* pe) {
-  const int li = l_index(kNT * E - 8);
-  if (A->pipe) {
-    lb_status_t st = launch_merge_pipe<E>(A, x, y, A->dev->pipe_grid[li], s);
+  const int li = l_index(L);
+  const int v = pipe_variant_for(L);
+  const bool ok = kVariants[v].kind == 0 ? A->vec : kVariants[v].kind == 1 ? A->pipe : A->vec32;
+  if (ok) {
+    lb_status_t st = kVariants[v].launch(A, x, y, A->dev->pipe_grid[v], s);
     if (st != LB_OK) return st;
     if (pe) { LB_CUDA(cudaEventRecord(pe->ev[2], s)); LB_CUDA(cudaEventRecord(pe->ev[3], s)); }
     return LB_OK;
   }
   int grid = 0;
-  lb_status_t st = A->vec ? launch_merge_tiles<E, true>(A, x, y, A->dev->fb_grid[li], &grid, s)
-                          : launch_merge_tiles<E, false>(A, x, y, A->dev->fb_grid[li], &grid, s);
+  lb_status_t st = A->vec ? launch_merge_tiles<L, true>(A, x, y, A->dev->fb_grid[li], &grid, s)
+                          : launch_merge_tiles<L, false>(A, x, y, A->dev->fb_grid[li], &grid, s);
   if (st != LB_OK) return st;
   if (pe) LB_CUDA(cudaEventRecord(pe->ev[2], s));
   lbk::fixup_kernel<<<(grid + kNT - 1) / kNT, kNT, 0, s>>>((int)A->rows, grid, A->carry_row, A->carry_val, y);
@@ -279,7 +422,6 @@ lb_status_t launch_merge(lb_csr_s* A, const float* x, float* y, stream_t s, Phas
   if (pe) LB_CUDA(cudaEventRecord(pe->ev[3], s));
   return LB_OK;
 }
-
 
 lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y, uint32_t flags, stream_t s,
                       PhaseEvents* pe) {
@@ -321,10 +463,11 @@ lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y
       }
       if (pe) LB_CUDA(cudaEventRecord(pe->ev[1], s));
       switch (A->L) {
-        case 1016: return launch_merge<4>(A, x, y, s, pe);
-        case 2040: return launch_merge<8>(A, x, y, s, pe);
-        case 3064: return launch_merge<12>(A, x, y, s, pe);
-        case 4088: return launch_merge<16>(A, x, y, s, pe);
+        case 504: return launch_merge<504>(A, x, y, s, pe);
+        case 1016: return launch_merge<1016>(A, x, y, s, pe);
+        case 2040: return launch_merge<2040>(A, x, y, s, pe);
+        case 3064: return launch_merge<3064>(A, x, y, s, pe);
+        case 4088: return launch_merge<4088>(A, x, y, s, pe);
         default: return fail(LB_ERR_INVALID_ARG, "unsupported tile length %d", A->L);
       }
     }
@@ -380,7 +523,7 @@ lb_status_t lb_csr_destroy(lb_csr_t A) {
 lb_status_t lb_csr_set_items_per_tile(lb_csr_t A, int32_t items_per_tile) {
   if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
   int L = items_per_tile == 0 ? LB_DEFAULT_ITEMS_PER_TILE : items_per_tile;
-  if (l_index(L) < 0) return fail(LB_ERR_INVALID_ARG, "items_per_tile %d unsupported (1016, 2040, 3064, 4088)", L);
+  if (l_index(L) < 0) return fail(LB_ERR_INVALID_ARG, "items_per_tile %d unsupported (504, 1016, 2040, 3064, 4088)", L);
   A->L = L;
   A->coords_valid = false;
   return LB_OK;

@@ -31,6 +31,17 @@ __device__ __forceinline__ float4 ld_cs_v4(const float* p) { return __ldcs(reint
 __device__ __forceinline__ int ld_cs(const int* p) { return __ldcs(p); }
 __device__ __forceinline__ float ld_cs(const float* p) { return __ldcs(p); }
 __device__ __forceinline__ float ld_x(const float* p) { return __ldg(p); }
+// x gather with an L2 evict_last policy (keeps x resident against the col/val stream)
+__device__ __forceinline__ float ld_x_keep(const float* p, uint64_t pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 
 // Segmented inclusive scan across a warp.  Pairs (f, v); combine(left, right) =
 // (left.f | right.f, right.f ? right.v : left.v + right.v).  With f = "a segment ended at or
@@ -415,8 +426,8 @@ __device__ __forceinline__ void pipe_issue(const PipeArgs& a, typename PipeCfg<N
   }
 }
 
-template <int NT, int E, int S>
-__global__ void __launch_bounds__(NT, 2) merge_pipe_kernel(PipeArgs a) {
+template <int NT, int E, int S, int MINB>
+__global__ void __launch_bounds__(NT, MINB) merge_pipe_kernel(PipeArgs a) {
   using Cfg = PipeCfg<NT, E, S>;
   constexpr int kW = Cfg::kWarps;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -567,6 +578,402 @@ __global__ void __launch_bounds__(NT, 2) merge_pipe_kernel(PipeArgs a) {
       float s = 0.f;
       for (int k = c; k < nc && __ldcg(a.carry_row + k) == r; ++k) s += __ldcg(a.carry_val + k);
       a.y[r] = __ldcg(a.y + r) + s;
+    }
+    if (tid == 0) *a.ticket = 0u;
+  }
+}
+
+// ----------------------------------------------------------------------------- merge-path tiles, direct (default)
+// The default tile processor.  On B200 every in-flight x[col] gather miss holds a 128-byte L1
+// line, so the gather rate follows the L1 capacity left over by shared memory
+// (profiles/r01_microbench_l1.txt: ~75 GNZ/s with 30 KB of L1, ~270 with 250 KB).  This kernel
+// therefore keeps shared memory to ~4 KB per CTA and streams the tile's col/val with coalesced
+// 128-bit loads straight into registers (thread t owns local nonzeros [4t, 4t+4), which makes
+// the per-thread contiguous layout and the coalesced layout the same thing), prefetching the
+// next tile's col/val/offsets while the current tile is reduced, and issuing the next tile's
+// gathers before the second barrier of the current one.
+struct DirectTile {
+  int i0, j0, i1, j1;   // tile coordinates
+  int4 col;             // this thread's 4 column indices (positions 4t..4t+3 from j0&~3)
+  float4 val;           // and values (0 outside [j0, j1))
+  int off_lo, off_hi;   // off[i0 + t], off[i0 + t + 1] for the row pass (t < rows of the tile)
+};
+
+template <int NT>
+__device__ __forceinline__ void direct_load(const PipeArgs& a, int t, int tid, DirectTile& d) {
+  const int2 c0 = a.coords[t], c1 = a.coords[t + 1];
+  d.i0 = c0.x; d.j0 = c0.y; d.i1 = c1.x; d.j1 = c1.y;
+  const int jA = d.j0 & ~3;
+  const int g = jA + 4 * tid;
+  if (g < d.j1 && g + 4 <= a.nnz) {
+    d.col = ld_cs_v4(a.col + g);
+    d.val = ld_cs_v4(a.val + g);
+  } else {
+    int c[4] = {0, 0, 0, 0};
+    float v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (g + e < d.j1) { c[e] = ld_cs(a.col + g + e); v[e] = ld_cs(a.val + g + e); }
+    d.col = make_int4(c[0], c[1], c[2], c[3]);
+    d.val = make_float4(v[0], v[1], v[2], v[3]);
+  }
+  const int nrows = d.i1 - d.i0;
+  if (tid < nrows) {
+    d.off_lo = __ldg(a.off + d.i0 + tid);
+    d.off_hi = __ldg(a.off + d.i0 + tid + 1);
+  }
+}
+
+// gathers for positions [lo, hi) of the tile (others contribute exactly 0)
+template <bool XKEEP>
+__device__ __forceinline__ void direct_gather(const PipeArgs& a, const DirectTile& d, int tid, float4& xv, float4& vv,
+                                              uint64_t xpol) {
+  const int jA = d.j0 & ~3;
+  const int q0 = 4 * tid, lo = d.j0 - jA, hi = d.j1 - jA;
+  const int cc[4] = {d.col.x, d.col.y, d.col.z, d.col.w};
+  const float vl[4] = {d.val.x, d.val.y, d.val.z, d.val.w};
+  float xr[4], vr[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const bool ok = q0 + e >= lo && q0 + e < hi;
+    xr[e] = ok ? (XKEEP ? ld_x_keep(a.x + cc[e], xpol) : ld_x(a.x + cc[e])) : 0.f;
+    vr[e] = ok ? vl[e] : 0.f;
+  }
+  xv = make_float4(xr[0], xr[1], xr[2], xr[3]);
+  vv = make_float4(vr[0], vr[1], vr[2], vr[3]);
+}
+
+template <int NT, int MINB, bool XKEEP>
+__global__ void __launch_bounds__(NT, MINB) merge_direct_kernel(PipeArgs a) {
+  constexpr int kW = NT / 32;
+  constexpr int kCap = 4 * NT;  // local nonzero positions per tile (L = kCap - 8)
+  __shared__ __align__(16) unsigned short s_tailrow[2][kCap];
+  __shared__ int s_cflag[kW];
+  __shared__ float s_cval[kW];
+  __shared__ int s_last;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t_begin = blockIdx.x * a.tiles_per_cta;
+  const int t_end = min(a.num_tiles, t_begin + a.tiles_per_cta);
+  const uint64_t xpol = XKEEP ? policy_evict_last() : 0ull;
+  for (int w = tid; w < 2 * kCap; w += NT) (&s_tailrow[0][0])[w] = 0;
+  // PDL: the prologue above overlapped the partition kernel; coords are read below.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __syncthreads();
+
+  // Three-stage software pipeline per thread: while tile t is reduced, tile t+1's gathers are
+  // in flight and tile t+2's col/val/offsets stream in from DRAM.
+  DirectTile cur, mid, nxt;         // tile t (gathered), t+1 (loaded, being gathered), t+2 (loading)
+  float4 xv_cur = make_float4(0.f, 0.f, 0.f, 0.f), vv_cur = xv_cur, xv_mid = xv_cur, vv_mid = xv_cur;
+  if (t_begin < t_end) direct_load<NT>(a, t_begin, tid, cur);
+  if (t_begin + 1 < t_end) direct_load<NT>(a, t_begin + 1, tid, mid);
+  if (t_begin < t_end) direct_gather<XKEEP>(a, cur, tid, xv_cur, vv_cur, xpol);
+
+  float cta_carry = 0.f;
+  int i_last = 0;
+  for (int t = t_begin; t < t_end; ++t) {
+    const int b = (t - t_begin) & 1;
+    const int i0 = cur.i0, nrows = cur.i1 - cur.i0;
+    const int jA = cur.j0 & ~3, lo = cur.j0 - jA;
+    // (1) row pass: mark each row's last nonzero, or write rows without a nonzero in the tile
+    for (int r = tid; r < nrows; r += NT) {
+      const int ob = r == tid ? cur.off_lo : __ldg(a.off + i0 + r);
+      const int oe = r == tid ? cur.off_hi : __ldg(a.off + i0 + r + 1);
+      const int e = oe - jA;
+      const int s = r == 0 ? lo : ob - jA;
+      if (e > s) s_tailrow[b][e - 1] = (unsigned short)(r + 1);
+      else a.y[i0 + r] = r == 0 ? cta_carry : 0.f;
+    }
+    // (2) gathers of tile t+1 (its col arrived during the previous tile), loads of tile t+2
+    if (t + 1 < t_end) direct_gather<XKEEP>(a, mid, tid, xv_mid, vv_mid, xpol);
+    if (t + 2 < t_end) direct_load<NT>(a, t + 2, tid, nxt);
+    __syncthreads();
+
+    // (3) this thread's 4 nonzeros: row sums, non-first row ends stored directly
+    const uint2 tr = *reinterpret_cast<const uint2*>(&s_tailrow[b][4 * tid]);
+    const unsigned rid[4] = {tr.x & 0xFFFFu, tr.x >> 16, tr.y & 0xFFFFu, tr.y >> 16};
+    const float xa[4] = {xv_cur.x, xv_cur.y, xv_cur.z, xv_cur.w};
+    const float va[4] = {vv_cur.x, vv_cur.y, vv_cur.z, vv_cur.w};
+    float run = 0.f, first_val = 0.f;
+    int first_r = -1;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      run = fmaf(va[e], xa[e], run);
+      if (rid[e]) {
+        const int r = (int)rid[e] - 1;
+        if (first_r < 0) { first_r = r; first_val = run; }
+        else a.y[i0 + r] = run;  // row started inside this thread (r > 0)
+        run = 0.f;
+      }
+    }
+    bool f = first_r >= 0;
+    float val = run;
+    warp_segscan_incl(f, val, (unsigned)lane);
+    float lval = __shfl_up_sync(kFull, val, 1);
+    const int lf = __shfl_up_sync(kFull, (int)f, 1);
+    const bool lflag = lane ? (bool)lf : false;
+    if (lane == 0) lval = 0.f;
+    if (lane == 31) { s_cflag[warp] = f; s_cval[warp] = val; }
+    __syncthreads();
+
+    // (4) warp-chunk scan; the first row end of each thread gets its carry-in
+    bool cf = lane < kW ? (bool)s_cflag[lane] : false;
+    float cv = lane < kW ? s_cval[lane] : 0.f;
+    warp_segscan_incl(cf, cv, (unsigned)lane);
+    const float agg_val = __shfl_sync(kFull, cv, kW - 1);
+    float ex_v = __shfl_up_sync(kFull, cv, 1);
+    if (lane == 0) ex_v = 0.f;
+    const float chunk_in = __shfl_sync(kFull, ex_v, warp);
+    if (first_r >= 0) {
+      float yv = (lflag ? lval : chunk_in + lval) + first_val;
+      if (first_r == 0) yv += cta_carry;
+      a.y[i0 + first_r] = yv;
+    }
+    if (tr.x | tr.y) *reinterpret_cast<uint2*>(&s_tailrow[b][4 * tid]) = make_uint2(0u, 0u);
+    cta_carry = nrows > 0 ? agg_val : cta_carry + agg_val;
+    i_last = cur.i1;
+    cur = mid;
+    xv_cur = xv_mid;
+    vv_cur = vv_mid;
+    mid = nxt;
+  }
+
+  // carry of this CTA's run; the last CTA to finish applies all carries (Alg.3 fix-up)
+  if (tid == 0) {
+    if (t_begin < t_end) {
+      a.carry_row[blockIdx.x] = i_last;
+      a.carry_val[blockIdx.x] = cta_carry;
+    }
+    __threadfence();
+    const unsigned done = atomicAdd(a.ticket, 1u);
+    s_last = done == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    const int nc = (int)gridDim.x;
+    for (int c = tid; c < nc; c += NT) {
+      const int r = __ldcg(a.carry_row + c);
+      if (r >= a.rows) continue;
+      if (c > 0 && __ldcg(a.carry_row + c - 1) == r) continue;
+      float sum = 0.f;
+      for (int k = c; k < nc && __ldcg(a.carry_row + k) == r; ++k) sum += __ldcg(a.carry_val + k);
+      a.y[r] = __ldcg(a.y + r) + sum;
+    }
+    if (tid == 0) *a.ticket = 0u;
+  }
+}
+
+// ----------------------------------------------------------------------------- merge-path tiles, wide
+// Like merge_direct_kernel but each thread owns E = 8 or 16 contiguous nonzeros of the tile, read
+// with 256-bit loads (sm_100a LDG.256, L1 no-allocate, L2 evict-first): the per-tile scans and
+// barriers are amortised over 2-4x more nonzeros, and a warp still reads whole 32-byte sectors.
+// Tile length L = NT*E - 8: the 32-byte-aligned nonzero range [j0&~7, j1) spans <= L + 7.
+__device__ __forceinline__ void ld_stream_v8(const int* p, int (&r)[8], uint64_t pol) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void ld_stream_v8(const float* p, float (&r)[8], uint64_t pol) {
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]), "=f"(r[6]), "=f"(r[7])
+               : "l"(p), "l"(pol));
+}
+
+template <int E>
+struct WideTile {
+  int i0, j0, i1, j1;
+  int col[E];
+  float val[E];
+  int off_lo, off_hi;
+};
+
+template <int NT, int E>
+__device__ __forceinline__ void wide_load(const PipeArgs& a, int4 c, int tid, WideTile<E>& d, uint64_t spol) {
+  d.i0 = c.x; d.j0 = c.y; d.i1 = c.z; d.j1 = c.w;  // coords prefetched one tile earlier
+  const int g = (d.j0 & ~7) + E * tid;
+  if (g < d.j1 && g + E <= a.nnz) {
+#pragma unroll
+    for (int k = 0; k < E / 8; ++k) {
+      int ci[8];
+      float vi[8];
+      ld_stream_v8(a.col + g + 8 * k, ci, spol);
+      ld_stream_v8(a.val + g + 8 * k, vi, spol);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) { d.col[8 * k + e] = ci[e]; d.val[8 * k + e] = vi[e]; }
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const bool ok = g + e < d.j1;
+      d.col[e] = ok ? ld_cs(a.col + g + e) : 0;
+      d.val[e] = ok ? ld_cs(a.val + g + e) : 0.f;
+    }
+  }
+  if (tid < d.i1 - d.i0) {
+    d.off_lo = __ldg(a.off + d.i0 + tid);
+    d.off_hi = __ldg(a.off + d.i0 + tid + 1);
+  }
+}
+
+// tile t's coordinates (i0, j0, i1, j1)
+__device__ __forceinline__ int4 tile_coords(const PipeArgs& a, int t) {
+  const int2 c0 = a.coords[t], c1 = a.coords[t + 1];
+  return make_int4(c0.x, c0.y, c1.x, c1.y);
+}
+
+// x gathers for valid positions; the gathered value replaces col (as float bits) to save registers
+template <int E>
+__device__ __forceinline__ void wide_gather(const PipeArgs& a, WideTile<E>& d, int tid, float (&xv)[E]) {
+  const int q0 = E * tid, lo = d.j0 & 7, hi = d.j1 - (d.j0 & ~7);
+  if (q0 >= lo && q0 + E <= hi) {  // interior thread: no masking
+#pragma unroll
+    for (int e = 0; e < E; ++e) xv[e] = ld_x(a.x + d.col[e]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const bool ok = q0 + e >= lo && q0 + e < hi;
+      xv[e] = ok ? ld_x(a.x + d.col[e]) : 0.f;
+      if (!ok) d.val[e] = 0.f;
+    }
+  }
+}
+
+// Segmented inclusive scan over the first N lanes only (N a power of two <= 32).
+template <int N>
+__device__ __forceinline__ void warp_segscan_incl_n(bool& f, float& v, unsigned lane) {
+#pragma unroll
+  for (int o = 1; o < N; o <<= 1) {
+    float vo = __shfl_up_sync(kFull, v, o);
+    int fo = __shfl_up_sync(kFull, (int)f, o);
+    if (lane >= (unsigned)o) {
+      if (!f) v = vo + v;
+      f = f || fo;
+    }
+  }
+}
+
+template <int NT, int E, int MINB>
+__global__ void __launch_bounds__(NT, MINB) merge_wide_kernel(PipeArgs a) {
+  constexpr int kW = NT / 32;
+  constexpr int kCap = E * NT;
+  static_assert(E == 8 || E == 16, "E");
+  __shared__ __align__(16) unsigned short s_tailrow[2][kCap];
+  __shared__ int s_cflag[kW];
+  __shared__ float s_cval[kW];
+  __shared__ int s_last;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t_begin = blockIdx.x * a.tiles_per_cta;
+  const int t_end = min(a.num_tiles, t_begin + a.tiles_per_cta);
+  const uint64_t spol = policy_evict_first();
+  for (int w = tid; w < 2 * kCap; w += NT) (&s_tailrow[0][0])[w] = 0;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: coords are read below
+  __syncthreads();
+
+  WideTile<E> cur, nxt;
+  float xv[E];
+  int4 c_next = make_int4(0, 0, 0, 0);  // coords of tile t+1 (prefetched during tile t-1)
+  if (t_begin < t_end) {
+    wide_load<NT, E>(a, tile_coords(a, t_begin), tid, cur, spol);
+    if (t_begin + 1 < t_end) c_next = tile_coords(a, t_begin + 1);
+    wide_gather<E>(a, cur, tid, xv);
+  }
+  float cta_carry = 0.f;
+  int i_last = 0;
+  // reduce tile t (`cur`, gathers in xv) while tile t+1 (`nxt`) streams in and gets gathered
+  for (int t = t_begin; t < t_end; ++t) {
+    const int b = (t - t_begin) & 1;
+    const int i0 = cur.i0, nrows = cur.i1 - cur.i0;
+    const int jA = cur.j0 & ~7, lo = cur.j0 - jA;
+    for (int r = tid; r < nrows; r += NT) {
+      const int ob = r == tid ? cur.off_lo : __ldg(a.off + i0 + r);
+      const int oe = r == tid ? cur.off_hi : __ldg(a.off + i0 + r + 1);
+      const int e = oe - jA;
+      const int s = r == 0 ? lo : ob - jA;
+      if (e > s) s_tailrow[b][e - 1] = (unsigned short)(r + 1);
+      else a.y[i0 + r] = r == 0 ? cta_carry : 0.f;
+    }
+    const bool has_next = t + 1 < t_end;
+    if (has_next) wide_load<NT, E>(a, c_next, tid, nxt, spol);
+    if (t + 2 < t_end) c_next = tile_coords(a, t + 2);
+    __syncthreads();
+
+    unsigned tr[E / 2];
+#pragma unroll
+    for (int k = 0; k < E / 8; ++k) {
+      const uint4 q = *reinterpret_cast<const uint4*>(&s_tailrow[b][E * tid + 8 * k]);
+      tr[4 * k] = q.x; tr[4 * k + 1] = q.y; tr[4 * k + 2] = q.z; tr[4 * k + 3] = q.w;
+    }
+    unsigned any = 0u;
+#pragma unroll
+    for (int k = 0; k < E / 2; ++k) any |= tr[k];
+    float run = 0.f, first_val = 0.f;
+    int first_r = -1;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      run = fmaf(cur.val[e], xv[e], run);
+      const unsigned rid = (e & 1) ? (tr[e >> 1] >> 16) : (tr[e >> 1] & 0xFFFFu);
+      if (rid) {
+        const int r = (int)rid - 1;
+        if (first_r < 0) { first_r = r; first_val = run; }
+        else a.y[i0 + r] = run;
+        run = 0.f;
+      }
+    }
+    bool f = first_r >= 0;
+    float val = run;
+    warp_segscan_incl(f, val, (unsigned)lane);
+    float lval = __shfl_up_sync(kFull, val, 1);
+    const int lf = __shfl_up_sync(kFull, (int)f, 1);
+    const bool lflag = lane ? (bool)lf : false;
+    if (lane == 0) lval = 0.f;
+    if (lane == 31) { s_cflag[warp] = f; s_cval[warp] = val; }
+    if (has_next) wide_gather<E>(a, nxt, tid, xv);  // next tile's gathers out before the barrier
+    __syncthreads();
+
+    bool cf = lane < kW ? (bool)s_cflag[lane] : false;
+    float cv = lane < kW ? s_cval[lane] : 0.f;
+    warp_segscan_incl_n<kW>(cf, cv, (unsigned)lane);
+    const float agg_val = __shfl_sync(kFull, cv, kW - 1);
+    float ex_v = __shfl_up_sync(kFull, cv, 1);
+    if (lane == 0) ex_v = 0.f;
+    const float chunk_in = __shfl_sync(kFull, ex_v, warp);
+    if (first_r >= 0) {
+      float yv = (lflag ? lval : chunk_in + lval) + first_val;
+      if (first_r == 0) yv += cta_carry;
+      a.y[i0 + first_r] = yv;
+    }
+    if (any) {
+#pragma unroll
+      for (int k = 0; k < E / 8; ++k)
+        *reinterpret_cast<uint4*>(&s_tailrow[b][E * tid + 8 * k]) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    cta_carry = nrows > 0 ? agg_val : cta_carry + agg_val;
+    i_last = cur.i1;
+    cur = nxt;
+  }
+
+  if (tid == 0) {
+    if (t_begin < t_end) {
+      a.carry_row[blockIdx.x] = i_last;
+      a.carry_val[blockIdx.x] = cta_carry;
+    }
+    __threadfence();
+    const unsigned done = atomicAdd(a.ticket, 1u);
+    s_last = done == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    const int nc = (int)gridDim.x;
+    for (int c = tid; c < nc; c += NT) {
+      const int r = __ldcg(a.carry_row + c);
+      if (r >= a.rows) continue;
+      if (c > 0 && __ldcg(a.carry_row + c - 1) == r) continue;
+      float sum = 0.f;
+      for (int k = c; k < nc && __ldcg(a.carry_row + k) == r; ++k) sum += __ldcg(a.carry_val + k);
+      a.y[r] = __ldcg(a.y + r) + sum;
     }
     if (tid == 0) *a.ticket = 0u;
   }

@@ -22,7 +22,7 @@ LB_OK, LB_ERR_INVALID_ARG, LB_ERR_INVALID_CSR, LB_ERR_UNSUPPORTED, LB_ERR_OOM, L
 SCHEDULES = {"thread_mapped": 0, "group_mapped": 1, "merge_path": 2, "block_mapped": 3}
 LB_SPMV_REPARTITION = 1
 DEFAULT_ITEMS_PER_TILE = 1016
-TILE_LENGTHS = (1016, 2040, 3064, 4088)
+TILE_LENGTHS = (504, 1016, 2040, 3064, 4088)
 
 
 class LbError(RuntimeError):

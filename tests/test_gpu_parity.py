@@ -114,7 +114,7 @@ def test_spmv_tolerance(name, sched):
     check_y(run(A, x, sched), y_ref, s_ref, False, f"{name}/{sched}")
 
 
-@pytest.mark.parametrize("L", [1016, 2040, 3064, 4088])
+@pytest.mark.parametrize("L", [504, 1016, 2040, 3064, 4088])
 @pytest.mark.parametrize("vmode", ["int", "float"])
 def test_merge_path_tile_lengths(L, vmode):
     A = lbgen.rmat(13, 16, 5, vmode)
@@ -370,3 +370,28 @@ def test_full_size_configs(cfg):
             check_y(yy, y_ref, s_ref, vmode == "int", f"{cfg}/{vmode}/{sched}")
         del M, A, x
         torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------- every tile-kernel variant
+VARIANTS = [(0, 1016), (1, 2040), (2, 4088), (3, 504), (4, 3064), (5, 1016), (6, 1016), (7, 504), (8, 504)]
+
+
+@pytest.mark.parametrize("variant,L", VARIANTS)
+def test_every_merge_variant(variant, L, monkeypatch):
+    """Each merge-path tile-kernel configuration (LB_PIPE_VARIANT) is bit-exact in integer mode
+    and within tolerance in float mode, on R-MAT, skewed and edge-case matrices."""
+    monkeypatch.setenv("LB_PIPE_VARIANT", str(variant))
+    cases = [("rmat", lambda vm: lbgen.rmat(13, 16, 5, vm)),
+             ("skewed", lambda vm: lbgen.skewed(1 << 12, 3, 30_000, 20_000, 8, vm)),
+             ("stencil", lambda vm: lbgen.stencil(70, 2, vm))]
+    for name, mk in cases:
+        for vm in ("int", "float"):
+            A = mk(vm)
+            x = lbgen.make_x(A.cols, vm, 9)
+            y_ref, s_ref = ref(A, x)
+            check_y(run(A, x, "merge_path", L), y_ref, s_ref, vm == "int", f"v{variant}/{name}/{vm}")
+    for name, A in {"giant": _csr([0, 100_003], 1), "no_nnz": _csr([0] * 3001, 3),
+                    "golden": _csr([0, 1, 3, 3, 6], 1)}.items():
+        x = torch.ones(A.cols)
+        y_ref, s_ref = ref(A, x)
+        check_y(run(A, x, "merge_path", L), y_ref, s_ref, True, f"v{variant}/{name}")
