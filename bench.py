@@ -65,14 +65,17 @@ def compulsory_bytes(rows, cols, nnz):
     return 8 * nnz + 4 * (rows + 1) + 4 * rows + 4 * cols
 
 
-def ncu_traffic(cfg, sched, L):
+def ncu_traffic(cfg, sched, L, kernel):
+    """DRAM bytes per launch of this kernel from a committed ncu --set full capture (or None)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
     e = d.get(f"{cfg}/{sched}/L{L}")
-    return None if e is None else e.get("dram_bytes_per_launch")
+    if e is None or e.get("kernel") != kernel.split(" ")[0]:
+        return None
+    return e.get("dram_bytes_per_launch")
 
 
 class ClockSampler:
@@ -251,9 +254,10 @@ def run_single(args, cfg):
                    "l2": "inputs (%.2f GB) larger than the 126 MB L2; no flush between steps" % (alg / 1e9)},
         "gpu_launches": int(launches),
         "phase_ms": {"partition": round(float(ph[0]), 5), "main": round(main_ms, 5), "fixup": round(float(ph[2]), 5)},
-        "roofline": {"bound": "hbm", "kernel": "merge_tile_kernel" if sched == "merge_path" else sched,
+        "roofline": {"bound": "hbm", "kernel": M.kernel_name(sched),
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": ncu_traffic(cfg, sched, args.items_per_tile), "algorithmic_bytes": alg,
+                     "traffic": ncu_traffic(cfg, sched, args.items_per_tile, M.kernel_name(sched)),
+                     "algorithmic_bytes": alg,
                      "peak_source": peak_src,
                      "kernel_ms_from": "mean of 20 lb_spmv_phase_times calls (CUDA events on the launch stream)"},
     }

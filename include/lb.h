@@ -199,6 +199,10 @@ lb_status_t lb_spmv_multi(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, co
  * d_y_full[b_r .. b_{r+1}) and receives every other rank's slice in place. */
 lb_status_t lb_allgather_rows(lb_comm_t c, const int64_t* h_bounds, float* d_y_full, void* stream);
 
+/* Name of the main kernel lb_spmv(A, sched) launches with the handle's current settings
+ * (diagnostics / bench reporting); "" for an unknown schedule. */
+const char* lb_kernel_name(lb_csr_t A, lb_schedule_t sched);
+
 /* Last error message of the calling thread ("" if none). */
 const char* lb_last_error(void);
 

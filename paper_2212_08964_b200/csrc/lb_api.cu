@@ -70,7 +70,7 @@ typedef lb_status_t (*pipe_prepare_fn)(int* blocks_per_sm);
 
 // One configuration of a merge-path tile kernel (kind 0: direct, kind 1: TMA-staged).
 struct PipeVariant {
-  int L, nt, e, minb, kind;
+  int L, nt, e, minb, kind;  // kind 0: merge_direct_kernel, 1: merge_pipe_kernel, 2: merge_wide_kernel
   pipe_prepare_fn prepare;
   pipe_launch_fn launch;
 };
@@ -482,6 +482,26 @@ lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y
 extern "C" {
 
 const char* lb_last_error(void) { return g_err.c_str(); }
+
+const char* lb_kernel_name(lb_csr_t A, lb_schedule_t sched) {
+  thread_local char buf[96];
+  switch (sched) {
+    case LB_SCHED_THREAD_MAPPED: return "thread_mapped_kernel";
+    case LB_SCHED_GROUP_MAPPED: return "group_mapped_kernel<32>";
+    case LB_SCHED_BLOCK_MAPPED: return "group_mapped_kernel<256>";
+    case LB_SCHED_MERGE_PATH: {
+      if (!A || l_index(A->L) < 0) return "";
+      const PipeVariant& v = kVariants[pipe_variant_for(A->L)];
+      const bool ok = v.kind == 0 ? A->vec : v.kind == 1 ? A->pipe : A->vec32;
+      if (!ok) { snprintf(buf, sizeof buf, "merge_tile_kernel<256,%d> + fixup_kernel", A->L); return buf; }
+      static const char* kinds[3] = {"merge_direct_kernel", "merge_pipe_kernel", "merge_wide_kernel"};
+      if (v.kind == 0) snprintf(buf, sizeof buf, "%s<%d,%d>", kinds[0], v.nt, v.minb);
+      else snprintf(buf, sizeof buf, "%s<%d,%d,%d>", kinds[v.kind], v.nt, v.e, v.minb);
+      return buf;
+    }
+    default: return "";
+  }
+}
 uint64_t lb_launch_count(void) { return g_launches.load(); }
 const char* lb_version(void) { return "liblb 0.1 (sm_100a)"; }
 

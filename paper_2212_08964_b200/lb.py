@@ -73,6 +73,7 @@ def lib() -> ctypes.CDLL:
         "lb_comm_destroy": ([p], st),
         "lb_spmv_multi": ([p, p, ctypes.c_int, p, p, p, p], st),
         "lb_allgather_rows": ([p, p, p, p], st),
+        "lb_kernel_name": ([p, ctypes.c_int], ctypes.c_char_p),
         "lb_last_error": ([], ctypes.c_char_p),
         "lb_launch_count": ([], ctypes.c_uint64),
         "lb_version": ([], ctypes.c_char_p),
@@ -205,6 +206,10 @@ class CsrMatrix:
                                 y.data_ptr() if self.rows else None, flags, _stream(stream)))
         return y
 
+    def kernel_name(self, schedule="merge_path") -> str:
+        """Main kernel lb_spmv launches for `schedule` (lb_kernel_name)."""
+        return lib().lb_kernel_name(self.handle, _sched(schedule)).decode()
+
     def phase_times(self, x: torch.Tensor, y: torch.Tensor, schedule="merge_path", stream=None) -> list[float]:
         """[partition, main, fixup] milliseconds of one call (lb_spmv_phase_times)."""
         ms = (ctypes.c_float * 3)()
@@ -251,6 +256,11 @@ def shard_bounds(row_offsets, nranks: int) -> np.ndarray:
     return out
 
 
+def gather_slices(bounds) -> list[tuple[int, int]]:
+    """The y slice [b_k, b_{k+1}) each rank k contributes to the all-gather (lb_allgather_rows)."""
+    return [(int(bounds[k]), int(bounds[k + 1])) for k in range(len(bounds) - 1)]
+
+
 def shard_csr(row_offsets: torch.Tensor, col_idx: torch.Tensor, values: torch.Tensor, bounds, rank: int):
     """Rows [b_r, b_{r+1}) of a CSR as its own CSR (offsets rebased to 0, global column ids).
     Returns fresh contiguous tensors on the same device (so 16-byte alignment holds)."""
@@ -276,14 +286,20 @@ class Comm:
         _check(lib().lb_comm_unique_id(buf))
         return bytes(buf)
 
+    @staticmethod
+    def bootstrap_uid() -> bytes:
+        """Rank 0 creates the NCCL unique id; torch.distributed (any backend) ships it to all ranks."""
+        import torch.distributed as dist
+        obj = [Comm.unique_id() if dist.get_rank() == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
     @classmethod
     def from_process_group(cls, device: int) -> "Comm":
-        """Bootstrap over torch.distributed (any backend): rank 0 makes the id, all ranks join."""
+        """Bootstrap over torch.distributed: rank 0 makes the id, all ranks join the communicator."""
         import torch.distributed as dist
-        rank, world = dist.get_rank(), dist.get_world_size()
-        obj = [cls.unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        return cls(obj[0], rank, world, device)
+        uid = cls.bootstrap_uid()
+        return cls(uid, dist.get_rank(), dist.get_world_size(), device)
 
     def close(self):
         if getattr(self, "_c", None):

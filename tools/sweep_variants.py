@@ -5,9 +5,7 @@ import numpy as np, torch
 import lbgen, oracle
 import paper_2212_08964_b200 as lb
 
-VARIANTS = [(26, 1016), (27, 1016), (29, 2040), (30, 2040), (31, 1016), (32, 504)]
-OLD = [
-            (9, 3064), (10, 4088), (11, 2040), (12, 504)]
+VARIANTS = [(0, 1016), (1, 2040), (2, 4088), (3, 504), (4, 3064), (5, 1016), (6, 1016), (7, 504), (8, 504)]
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
 # correctness on a small int matrix
 As = lbgen.rmat(13, 16, 5, "int"); xs = lbgen.make_x(As.cols, "int", 3)
