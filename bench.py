@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip e2e / cpu_baseline / clocks (profiling runs)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="budget for the cpu_baseline sample")
+    ap.add_argument("--multi", action="store_true", help="use the multi-GPU step even at world size 1 (testing)")
     return ap.parse_args()
 
 
@@ -297,7 +298,9 @@ def run_multi(args, cfg):
     world, rank, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29517")
+    dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     A = lbgen.make_config(cfg, "float", device=dev)
     x = lbgen.x_for_config(cfg, A.cols, "float", device=dev)
     rows, cols, nnz = A.rows, A.cols, A.nnz
@@ -373,7 +376,7 @@ def main():
         cfg = args.config or ("c3" if world == 1 else "c5")
         run_reference(args, cfg)
         return
-    if world > 1:
+    if world > 1 or args.multi:
         run_multi(args, args.config or "c5")
     else:
         run_single(args, args.config or "c3")

@@ -65,20 +65,29 @@ typedef enum {
  *                  P:1018-1028 [Sec. Merge-path load balancing]).
  *  BLOCK_MAPPED    GROUP_MAPPED with G = 256 (a CTA) -- the block-mapped instance the paper gets
  *                  "for free" from the group-mapped schedule (table).
+ *  AUTO            the paper's heuristic: merge-path unless (rows < alpha or cols < alpha)
+ *                  and nnz < beta (alpha = 500, beta = 10000), then thread-mapped; extended with a
+ *                  row-regularity test for B200 (reading R18): thread-mapped when the longest row
+ *                  is at most 2 x mean + 8 and the mean is <= 32 nonzeros.  The row-length maximum
+ *                  is computed once per handle by a reduction kernel (first AUTO call; one sync).
  */
 typedef enum {
   LB_SCHED_THREAD_MAPPED = 0,
   LB_SCHED_GROUP_MAPPED = 1,
   LB_SCHED_MERGE_PATH = 2,
-  LB_SCHED_BLOCK_MAPPED = 3
+  LB_SCHED_BLOCK_MAPPED = 3,
+  LB_SCHED_AUTO = 4
 } lb_schedule_t;
+
 
 typedef struct lb_csr_s* lb_csr_t;   /* opaque CSR handle (borrowed arrays + owned scratch) */
 typedef struct lb_comm_s* lb_comm_t; /* opaque multi-GPU communicator (wraps an ncclComm_t) */
 
-/* Default merge-path tile length L (merge items per tile) used by lb_spmv.  Supported lengths are
- * L = NT*E - 8 for NT threads x E nonzeros per thread (E a multiple of 4): a tile's 16-byte-aligned range
- * of nonzeros spans at most L + 6 elements, so every thread of the CTA gets E of them. */
+/* Merge-path tile length L (merge items per tile).  Supported lengths are 504, 1016, 2040, 3064 and
+ * 4088 (= 256*R - 8 or NT*E - 8: a tile's 32-byte-aligned range of nonzeros spans at most L + 7
+ * elements, so every lane of the processing warp/CTA gets the same number of slots).  The handle's
+ * default is chosen from the shape at lb_csr_create: 2040 when nnz < 8*rows (short rows), else
+ * 1016.  LB_DEFAULT_ITEMS_PER_TILE is the long-row default. */
 #define LB_DEFAULT_ITEMS_PER_TILE 1016
 
 /*
@@ -102,7 +111,7 @@ lb_status_t lb_csr_destroy(lb_csr_t A);
 
 /*
  * lb_csr_set_items_per_tile -- choose the merge-path tile length L used by lb_spmv
- * (0 = LB_DEFAULT_ITEMS_PER_TILE).  Supported: 504, 1016, 2040, 3064, 4088; anything else returns
+ * (0 = the shape-based default described at LB_DEFAULT_ITEMS_PER_TILE).  Supported: 504, 1016, 2040, 3064, 4088; anything else returns
  * LB_ERR_INVALID_ARG.
  * Invalidates the cached partition.  Not thread-safe with respect to in-flight lb_spmv.
  */
@@ -134,6 +143,10 @@ lb_status_t lb_partition(lb_csr_t A, int32_t items_per_tile, int32_t* d_coords, 
  * identical results for identical inputs and launch configuration).
  */
 lb_status_t lb_spmv(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_y, void* stream);
+
+/* lb_select_schedule -- the concrete schedule LB_SCHED_AUTO resolves to for this handle (computes
+ * and caches the row statistics on first use: one reduction kernel + one sync of `stream`). */
+lb_status_t lb_select_schedule(lb_csr_t A, void* stream, lb_schedule_t* out);
 
 /* Flags for lb_spmv_ex. */
 #define LB_SPMV_REPARTITION 1u /* MERGE_PATH: recompute the partition inside this call */

@@ -125,23 +125,46 @@ template <int NT, int E, int MINB>
 lb_status_t wide_launch(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s);
 #define LB_WIDE_VARIANT(NT, E, MINB) {NT * E - 8, NT, E, MINB, 2, wide_prepare<NT, E, MINB>, wide_launch<NT, E, MINB>}
 
+template <int W, int R, int MINB>
+lb_status_t stream_prepare(int* blocks) {
+  auto k = lbk::merge_stream_kernel<W, R, MINB>;
+  cudaFuncAttributes fa;
+  LB_CUDA(cudaFuncGetAttributes(&fa, k));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k, W * 32, 0));
+  const double need = (double)(*blocks) * (fa.sharedSizeBytes + 1024);
+  int pct = (int)(100.0 * need / (228.0 * 1024.0)) + 1;
+  pct = std::min(100, std::max(1, pct));
+  LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k, W * 32, 0));
+  return LB_OK;
+}
+template <int W, int R, int MINB>
+lb_status_t stream_launch(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s);
+// warp-streamed tiles: L = 256*R - 8, W warps per CTA (nt = W*32, e = 8 nonzeros per lane per round)
+#define LB_STREAM_VARIANT(W, R, MINB) \
+  {256 * R - 8, W * 32, 8, MINB, 3, stream_prepare<W, R, MINB>, stream_launch<W, R, MINB>}
+
 #define LB_DIRECT_VARIANT(NT, MINB, XK) \
   {NT * 4 - 8, NT, 4, MINB, 0, direct_prepare<NT, MINB, XK>, direct_launch<NT, MINB, XK>}
 #define LB_PIPE_VARIANT(NT, E, MINB) {NT * E - 8, NT, E, MINB, 1, pipe_prepare<NT, E, MINB>, pipe_launch<NT, E, MINB>}
 const PipeVariant kVariants[] = {
-    LB_WIDE_VARIANT(128, 8, 8),        // 0 L=1016  default (C3 R-MAT, C4 skewed: best measured)
-    LB_WIDE_VARIANT(256, 8, 4),        // 1 L=2040  default (C2 stencil: best measured)
-    LB_WIDE_VARIANT(256, 16, 2),       // 2 L=4088  default
-    LB_DIRECT_VARIANT(128, 8, false),  // 3 L=504   default
-    LB_PIPE_VARIANT(256, 12, 2),       // 4 L=3064  default (TMA-staged)
-    LB_PIPE_VARIANT(256, 4, 2),        // 5 L=1016  alternative: TMA bulk-copy staging of col/val/off
-    LB_DIRECT_VARIANT(256, 2, false),  // 6 L=1016  alternative: 128-bit loads, 4 nonzeros per thread
-    LB_WIDE_VARIANT(64, 8, 16),        // 7 L=504   alternative
-    LB_DIRECT_VARIANT(128, 4, true),   // 8 L=504   alternative: x gathers with L2 evict_last
+    LB_STREAM_VARIANT(8, 4, 2),        // 0  L=1016 default: warp-streamed (C3 R-MAT, C4 skewed: best measured)
+    LB_WIDE_VARIANT(256, 8, 4),        // 1  L=2040 default: CTA tiles, 8 nonzeros/thread (C2 stencil: best)
+    LB_WIDE_VARIANT(256, 16, 2),       // 2  L=4088 default
+    LB_STREAM_VARIANT(4, 2, 4),        // 3  L=504  default
+    LB_PIPE_VARIANT(256, 12, 2),       // 4  L=3064 default (TMA-staged)
+    LB_PIPE_VARIANT(256, 4, 2),        // 5  L=1016 alternative: TMA bulk-copy staging of col/val/off
+    LB_DIRECT_VARIANT(256, 2, false),  // 6  L=1016 alternative: 128-bit loads, 4 nonzeros per thread
+    LB_DIRECT_VARIANT(128, 8, false),  // 7  L=504  alternative
+    LB_DIRECT_VARIANT(128, 4, true),   // 8  L=504  alternative: x gathers with L2 evict_last
+    LB_WIDE_VARIANT(128, 8, 8),        // 9  L=1016 alternative: CTA tiles, 8 nonzeros/thread
+    LB_STREAM_VARIANT(4, 4, 4),        // 10 L=1016 alternative: warp-streamed, 4 warps/CTA
+    LB_STREAM_VARIANT(4, 8, 4),        // 11 L=2040 alternative: warp-streamed
+    LB_WIDE_VARIANT(64, 8, 16),        // 12 L=504  alternative
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 // default variant per tile length (index into kVariants), chosen by measurement
-constexpr int kDefaultVariant[kNumL] = {3, 0, 1, 4, 2};  // per kTileL entry
+constexpr int kDefaultVariant[kNumL] = {3, 0, 1, 4, 2};  // per kTileL entry (504, 1016, 2040, 3064, 4088)
 
 struct DeviceInfo {
   int sm_count = 0;
@@ -225,6 +248,7 @@ struct lb_csr_s {
   float* carry_val = nullptr; // [kMaxCtas]
   int* flags = nullptr;       // [4] validation flags
   unsigned* ticket = nullptr; // [1] last-CTA ticket of the pipelined kernel (kept at 0 between launches)
+  int max_row = -1;           // longest row (LB_SCHED_AUTO), -1 until computed
 };
 
 namespace {
@@ -250,6 +274,11 @@ void carve_scratch(lb_csr_s* A, char* p) {
   A->ticket = reinterpret_cast<unsigned*>(p);
 }
 
+// Default tile length from the matrix shape (measured on B200): matrices with
+// short rows (< 8 nonzeros per row on average, e.g. stencils) run best on the CTA-tile kernel
+// with L = 2040; longer / irregular rows on the warp-streamed kernel with L = 1016.
+int auto_tile_length(int64_t rows, int64_t nnz) { return nnz < 8 * rows ? 2040 : 1016; }
+
 lb_status_t check_shape(int64_t rows, int64_t cols, int64_t nnz) {
   if (rows < 0 || cols < 0 || nnz < 0) return fail(LB_ERR_INVALID_ARG, "negative size (rows=%lld cols=%lld nnz=%lld)",
                                                    (long long)rows, (long long)cols, (long long)nnz);
@@ -269,6 +298,7 @@ lb_status_t init_handle(lb_csr_s* A, int64_t rows, int64_t cols, int64_t nnz, co
   A->vec = (reinterpret_cast<uintptr_t>(col) % 16 == 0) && (reinterpret_cast<uintptr_t>(val) % 16 == 0);
   A->pipe = A->vec && (reinterpret_cast<uintptr_t>(off) % 16 == 0);
   A->vec32 = (reinterpret_cast<uintptr_t>(col) % 32 == 0) && (reinterpret_cast<uintptr_t>(val) % 32 == 0);
+  A->L = auto_tile_length(rows, nnz);
   return LB_OK;
 }
 
@@ -401,11 +431,39 @@ lb_status_t wide_launch(lb_csr_s* A, const float* x, float* y, int grid_max, str
   return LB_OK;
 }
 
+template <int W, int R, int MINB>
+lb_status_t stream_launch(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s) {
+  constexpr int L = 256 * R - 8;
+  const int T = (int)num_tiles(A->rows, A->nnz, L);
+  const int warps_max = std::min(grid_max * W, kMaxCtas);
+  const int tpw = (T + warps_max - 1) / warps_max;   // tiles per warp
+  const int warps = (T + tpw - 1) / tpw;
+  const int grid = (warps + W - 1) / W;
+  lbk::PipeArgs a;
+  a.off = A->off; a.col = A->col; a.val = A->val; a.x = x; a.y = y;
+  a.coords = A->coords; a.rows = (int)A->rows; a.nnz = (int)A->nnz;
+  a.num_tiles = T; a.tiles_per_cta = tpw;
+  a.carry_row = A->carry_row; a.carry_val = A->carry_val; a.ticket = A->ticket;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(W * 32);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL after lb_partition
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LB_CUDA(cudaLaunchKernelEx(&cfg, lbk::merge_stream_kernel<W, R, MINB>, a));
+  LB_LAUNCHED();
+  return LB_OK;
+}
+
 template <int L>
 lb_status_t launch_merge(lb_csr_s* A, const float* x, float* y, stream_t s, PhaseEvents* pe) {
   const int li = l_index(L);
   const int v = pipe_variant_for(L);
-  const bool ok = kVariants[v].kind == 0 ? A->vec : kVariants[v].kind == 1 ? A->pipe : A->vec32;
+  const bool ok = kVariants[v].kind == 0 ? A->vec : kVariants[v].kind == 1 ? A->pipe : A->vec32;  // 2, 3: 256-bit
   if (ok) {
     lb_status_t st = kVariants[v].launch(A, x, y, A->dev->pipe_grid[v], s);
     if (st != LB_OK) return st;
@@ -423,12 +481,37 @@ lb_status_t launch_merge(lb_csr_s* A, const float* x, float* y, stream_t s, Phas
   return LB_OK;
 }
 
+// LB_SCHED_AUTO (reading R18): the paper's alpha/beta rule + a row-regularity test.
+lb_status_t select_schedule(lb_csr_s* A, stream_t s, lb_schedule_t* out) {
+  const int64_t alpha = 500, beta = 10000;
+  if ((A->rows < alpha || A->cols < alpha) && A->nnz < beta) { *out = LB_SCHED_THREAD_MAPPED; return LB_OK; }
+  if (A->rows == 0) { *out = LB_SCHED_MERGE_PATH; return LB_OK; }
+  if (A->max_row < 0) {
+    LB_CUDA(cudaMemsetAsync(A->flags, 0, sizeof(int), s));
+    const int grid = (int)std::min<int64_t>((A->rows + kNT - 1) / kNT, (int64_t)A->dev->sm_count * 8);
+    lbk::max_row_kernel<<<std::max(grid, 1), kNT, 0, s>>>((int)A->rows, A->off, A->flags);
+    LB_LAUNCHED();
+    int m = 0;
+    LB_CUDA(cudaMemcpyAsync(&m, A->flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LB_CUDA(cudaStreamSynchronize(s));
+    A->max_row = m;
+  }
+  const double mean = (double)A->nnz / (double)A->rows;
+  const bool regular = A->max_row <= 2.0 * mean + 8.0 && mean <= 32.0;
+  *out = regular ? LB_SCHED_THREAD_MAPPED : LB_SCHED_MERGE_PATH;
+  return LB_OK;
+}
+
 lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y, uint32_t flags, stream_t s,
                       PhaseEvents* pe) {
   if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
   if (A->rows == 0) return LB_OK;
   if (!y || (!x && A->nnz > 0)) return fail(LB_ERR_INVALID_ARG, "null x or y");
   if ((const void*)x == (const void*)y) return fail(LB_ERR_INVALID_ARG, "x and y must not alias");
+  if (sched == LB_SCHED_AUTO) {
+    lb_status_t st = select_schedule(A, s, &sched);
+    if (st != LB_OK) return st;
+  }
   if (pe) LB_CUDA(cudaEventRecord(pe->ev[0], s));
   switch (sched) {
     case LB_SCHED_THREAD_MAPPED: {
@@ -483,8 +566,15 @@ extern "C" {
 
 const char* lb_last_error(void) { return g_err.c_str(); }
 
+lb_status_t lb_select_schedule(lb_csr_t A, void* stream, lb_schedule_t* out) {
+  g_err.clear();
+  if (!A || !out) return fail(LB_ERR_INVALID_ARG, "null argument");
+  return select_schedule(A, S(stream), out);
+}
+
 const char* lb_kernel_name(lb_csr_t A, lb_schedule_t sched) {
   thread_local char buf[96];
+  if (sched == LB_SCHED_AUTO && A && A->max_row >= 0) select_schedule(A, nullptr, &sched);
   switch (sched) {
     case LB_SCHED_THREAD_MAPPED: return "thread_mapped_kernel";
     case LB_SCHED_GROUP_MAPPED: return "group_mapped_kernel<32>";
@@ -494,8 +584,10 @@ const char* lb_kernel_name(lb_csr_t A, lb_schedule_t sched) {
       const PipeVariant& v = kVariants[pipe_variant_for(A->L)];
       const bool ok = v.kind == 0 ? A->vec : v.kind == 1 ? A->pipe : A->vec32;
       if (!ok) { snprintf(buf, sizeof buf, "merge_tile_kernel<256,%d> + fixup_kernel", A->L); return buf; }
-      static const char* kinds[3] = {"merge_direct_kernel", "merge_pipe_kernel", "merge_wide_kernel"};
+      static const char* kinds[4] = {"merge_direct_kernel", "merge_pipe_kernel", "merge_wide_kernel",
+                                     "merge_stream_kernel"};
       if (v.kind == 0) snprintf(buf, sizeof buf, "%s<%d,%d>", kinds[0], v.nt, v.minb);
+      else if (v.kind == 3) snprintf(buf, sizeof buf, "%s<%d,%d,%d>", kinds[3], v.nt / 32, (v.L + 8) / 256, v.minb);
       else snprintf(buf, sizeof buf, "%s<%d,%d,%d>", kinds[v.kind], v.nt, v.e, v.minb);
       return buf;
     }
@@ -542,7 +634,7 @@ lb_status_t lb_csr_destroy(lb_csr_t A) {
 
 lb_status_t lb_csr_set_items_per_tile(lb_csr_t A, int32_t items_per_tile) {
   if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
-  int L = items_per_tile == 0 ? LB_DEFAULT_ITEMS_PER_TILE : items_per_tile;
+  int L = items_per_tile == 0 ? auto_tile_length(A->rows, A->nnz) : items_per_tile;
   if (l_index(L) < 0) return fail(LB_ERR_INVALID_ARG, "items_per_tile %d unsupported (504, 1016, 2040, 3064, 4088)", L);
   A->L = L;
   A->coords_valid = false;

@@ -87,6 +87,16 @@ __global__ void validate_kernel(int rows, int cols, int nnz, const int* __restri
   }
 }
 
+// max row length (for LB_SCHED_AUTO): grid-stride max over off[r+1]-off[r], one atomicMax per warp
+__global__ void max_row_kernel(int rows, const int* __restrict__ off, int* out) {
+  int m = 0;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+    m = max(m, __ldg(off + r + 1) - __ldg(off + r));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(kFull, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 // ----------------------------------------------------------------------------- partition
 // Alg.3 P:306-311 (2DSearch) for every tile boundary t = 0..T:
 //   d = min(t*L, rows+nnz);  i = #{k < rows : k + off[k+1] < d};  j = d - i.
@@ -976,6 +986,235 @@ __global__ void __launch_bounds__(NT, MINB) merge_wide_kernel(PipeArgs a) {
       a.y[r] = __ldcg(a.y + r) + sum;
     }
     if (tid == 0) *a.ticket = 0u;
+  }
+}
+
+// ----------------------------------------------------------------------------- merge-path tiles, warp-streamed
+// Each WARP owns a contiguous run of merge-path tiles (tile length L = 256*R - 8) and streams
+// them as rounds of 256 nonzeros (8 contiguous per lane, 256-bit loads).  A 3-deep register
+// pipeline keeps round r+2 loading and round r+1's x gathers in flight while round r is
+// reduced; the partial sum of the open row flows from round to round (and tile to tile) in a
+// warp-uniform register, so there is no CTA barrier in the main loop and one warp segmented scan
+// per 256 nonzeros.  The row pass of tile t+1 runs at the end of tile t from prefetched offsets
+// and marks each row's last nonzero in a per-warp shared buffer.
+template <int R>
+struct StreamCfg {
+  static constexpr int kCap = 256 * R;  // local nonzero positions per tile
+  static constexpr int L = kCap - 8;    // merge items per tile
+  static constexpr int K = 2;           // rows per lane whose offsets are prefetched (64 rows / tile)
+};
+
+struct StreamRound {  // one round's data for one lane
+  int col[8];
+  float val[8];
+};
+
+__device__ __forceinline__ void stream_load(const PipeArgs& a, int4 c, int k, int lane, StreamRound& d,
+                                            uint64_t spol) {
+  const int g = (c.y & ~7) + 256 * k + 8 * lane;
+  if (g < c.w && g + 8 <= a.nnz) {
+    ld_stream_v8(a.col + g, d.col, spol);
+    ld_stream_v8(a.val + g, d.val, spol);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const bool ok = g + e < c.w;
+      d.col[e] = ok ? ld_cs(a.col + g + e) : 0;
+      d.val[e] = ok ? ld_cs(a.val + g + e) : 0.f;
+    }
+  }
+}
+
+// gathers x for the round's valid positions; invalid positions get val = 0 (they add exactly 0)
+__device__ __forceinline__ void stream_gather(const PipeArgs& a, int4 c, int k, int lane, StreamRound& d,
+                                              float (&xv)[8]) {
+  const int q0 = 256 * k + 8 * lane, lo = c.y & 7, hi = c.w - (c.y & ~7);
+  if (q0 >= lo && q0 + 8 <= hi) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) xv[e] = ld_x(a.x + d.col[e]);
+  } else {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const bool ok = q0 + e >= lo && q0 + e < hi;
+      xv[e] = ok ? ld_x(a.x + d.col[e]) : 0.f;
+      if (!ok) d.val[e] = 0.f;
+    }
+  }
+}
+
+template <int R, int K>
+__device__ __forceinline__ void stream_prefetch_offsets(const PipeArgs& a, int4 c, int lane, int (&lo_)[K],
+                                                        int (&hi_)[K]) {
+  const int nrows = c.z - c.x;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    const int r = lane + 32 * j;
+    if (r < nrows) {
+      lo_[j] = __ldg(a.off + c.x + r);
+      hi_[j] = __ldg(a.off + c.x + r + 1);
+    }
+  }
+}
+
+// Row pass of tile c into tail[]: tail[q] = r + 1 when local nonzero q ends row r (r >= 0);
+// rows r > 0 with no nonzero in the tile get y = 0; returns (warp-uniform) whether row 0 has no
+// nonzero in the tile (its value is then the carry entering the tile).
+template <int R, int K>
+__device__ __forceinline__ bool stream_row_pass(const PipeArgs& a, int4 c, int lane, const int (&lo_)[K],
+                                                const int (&hi_)[K], unsigned short* tail) {
+  const int i0 = c.x, nrows = c.z - c.x, jA = c.y & ~7, lo = c.y - jA;
+  bool row0_empty = false;
+  for (int j = 0; 32 * j < nrows; ++j) {
+    const int r = lane + 32 * j;
+    if (r < nrows) {
+      int ob, oe;
+      if (j < K) {
+#pragma unroll
+        for (int q = 0; q < K; ++q)
+          if (q == j) { ob = lo_[q]; oe = hi_[q]; }
+      } else {
+        ob = __ldg(a.off + i0 + r);
+        oe = __ldg(a.off + i0 + r + 1);
+      }
+      const int e = oe - jA;
+      const int s = r == 0 ? lo : ob - jA;
+      if (e > s) tail[e - 1] = (unsigned short)(r + 1);
+      else if (r > 0) a.y[i0 + r] = 0.f;
+      else row0_empty = true;
+    }
+  }
+  return __shfl_sync(kFull, (int)row0_empty, 0) != 0;
+}
+
+template <int W, int R, int MINB>
+__global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) {
+  using Cfg = StreamCfg<R>;
+  constexpr int K = Cfg::K;
+  __shared__ __align__(16) unsigned short s_tail[W][Cfg::kCap];
+  __shared__ int s_last;
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * W + warp;  // global warp id: owns tiles [t_begin, t_end)
+  const int t_begin = min(a.num_tiles, gw * a.tiles_per_cta);
+  const int t_end = min(a.num_tiles, t_begin + a.tiles_per_cta);
+  const uint64_t spol = policy_evict_first();
+  unsigned short* tail = s_tail[warp];
+  for (int w = lane; w < Cfg::kCap / 8; w += 32) reinterpret_cast<uint4*>(tail)[w] = make_uint4(0u, 0u, 0u, 0u);
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: coords are read below
+  __syncwarp();
+
+  float rc = 0.f;  // partial sum of the row open at the current stream position (warp-uniform)
+  int i_last = t_begin < t_end ? __ldg(&a.coords[t_end].x) : a.rows;
+  if (t_begin < t_end) {
+    const int nsteps = (t_end - t_begin) * R;
+    // coordinates of tiles t, t+1, t+2 (int4 = i0, j0, i1, j1)
+    int4 cT = tile_coords(a, t_begin);
+    int4 cT1 = t_begin + 1 < t_end ? tile_coords(a, t_begin + 1) : cT;
+    int4 cT2 = t_begin + 2 < t_end ? tile_coords(a, t_begin + 2) : cT1;
+    int olo[K], ohi[K];
+    stream_prefetch_offsets<R, K>(a, cT, lane, olo, ohi);
+    bool r0e = stream_row_pass<R, K>(a, cT, lane, olo, ohi, tail);
+    if (t_begin + 1 < t_end) stream_prefetch_offsets<R, K>(a, cT1, lane, olo, ohi);
+    __syncwarp();
+    // pipeline registers: step s (gathered), s+1 (gathered next), s+2 (loading)
+    StreamRound d0, d1, d2;
+    float x0[8], x1[8];
+    stream_load(a, cT, 0, lane, d0, spol);
+    if (1 < nsteps) stream_load(a, R > 1 ? cT : cT1, R > 1 ? 1 : 0, lane, d1, spol);
+    stream_gather(a, cT, 0, lane, d0, x0);
+
+    int t = t_begin, k = 0;
+    for (int st = 0; st < nsteps; ++st) {
+      // (a) gathers for step st+1, loads for step st+2
+      if (st + 1 < nsteps) {
+        const bool same = k + 1 < R;
+        stream_gather(a, same ? cT : cT1, same ? k + 1 : k + 1 - R, lane, d1, x1);
+      }
+      if (st + 2 < nsteps) {
+        const int k2 = k + 2;
+        const bool same = k2 < R;
+        stream_load(a, same ? cT : cT1, same ? k2 : k2 - R, lane, d2, spol);
+      }
+      // (b) the row open at the tile start has no nonzero here: it ends now with the carry
+      const int i0 = cT.x;
+      if (k == 0 && r0e) {
+        if (lane == 0) a.y[i0] = rc;
+        rc = 0.f;
+      }
+      // (c) reduce this round
+      const uint4 tq = *reinterpret_cast<const uint4*>(&tail[256 * k + 8 * lane]);
+      const unsigned tr[4] = {tq.x, tq.y, tq.z, tq.w};
+      float run = 0.f, first_val = 0.f;
+      int first_r = -1;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        run = fmaf(d0.val[e], x0[e], run);
+        const unsigned rid = (e & 1) ? (tr[e >> 1] >> 16) : (tr[e >> 1] & 0xFFFFu);
+        if (rid) {
+          const int r = (int)rid - 1;
+          if (first_r < 0) { first_r = r; first_val = run; }
+          else a.y[i0 + r] = run;  // row started inside this lane's 8 nonzeros
+          run = 0.f;
+        }
+      }
+      bool f = first_r >= 0;
+      float v = run;
+      warp_segscan_incl(f, v, (unsigned)lane);
+      float lval = __shfl_up_sync(kFull, v, 1);
+      const int lf = __shfl_up_sync(kFull, (int)f, 1);
+      const int agg_f = __shfl_sync(kFull, (int)f, 31);
+      const float agg_v = __shfl_sync(kFull, v, 31);
+      if (first_r >= 0) {
+        const float carry_in = lane == 0 ? rc : (lf ? lval : rc + lval);
+        a.y[i0 + first_r] = carry_in + first_val;
+      }
+      if (tr[0] | tr[1] | tr[2] | tr[3])
+        *reinterpret_cast<uint4*>(&tail[256 * k + 8 * lane]) = make_uint4(0u, 0u, 0u, 0u);
+      rc = agg_f ? agg_v : rc + agg_v;
+      // (d) rotate the pipeline
+#pragma unroll
+      for (int e = 0; e < 8; ++e) { d0.val[e] = d1.val[e]; x0[e] = x1[e]; d1.col[e] = d2.col[e]; d1.val[e] = d2.val[e]; }
+      if (++k == R) {  // tile t done: row pass of tile t+1 (offsets prefetched), advance coords
+        k = 0;
+        ++t;
+        __syncwarp();
+        if (t < t_end) {
+          r0e = stream_row_pass<R, K>(a, cT1, lane, olo, ohi, tail);
+          if (t + 1 < t_end) stream_prefetch_offsets<R, K>(a, cT2, lane, olo, ohi);
+          cT = cT1;
+          cT1 = cT2;
+          if (t + 2 < t_end) cT2 = tile_coords(a, t + 2);
+        }
+      }
+      __syncwarp();
+    }
+  }
+
+  // one carry per warp (rows == a.rows for warps without tiles: skipped by the fix-up), then the
+  // last CTA to finish applies all carries in warp order (Alg.3 fix-up, deterministic)
+  if (lane == 0) {
+    a.carry_row[gw] = i_last;
+    a.carry_val[gw] = rc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned done = atomicAdd(a.ticket, 1u);
+    s_last = done == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    const int nc = (int)gridDim.x * W;
+    for (int c = threadIdx.x; c < nc; c += W * 32) {
+      const int r = __ldcg(a.carry_row + c);
+      if (r >= a.rows) continue;
+      if (c > 0 && __ldcg(a.carry_row + c - 1) == r) continue;
+      float sum = 0.f;
+      for (int kk = c; kk < nc && __ldcg(a.carry_row + kk) == r; ++kk) sum += __ldcg(a.carry_val + kk);
+      a.y[r] = __ldcg(a.y + r) + sum;
+    }
+    if (threadIdx.x == 0) *a.ticket = 0u;
   }
 }
 

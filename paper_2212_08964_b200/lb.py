@@ -19,7 +19,8 @@ LIB_PATH = os.environ.get("LB_LIB_PATH") or os.path.join(_PKG, "liblb.so")
 HEADER = os.path.join(_ROOT, "include", "lb.h")
 
 LB_OK, LB_ERR_INVALID_ARG, LB_ERR_INVALID_CSR, LB_ERR_UNSUPPORTED, LB_ERR_OOM, LB_ERR_CUDA, LB_ERR_NCCL = range(7)
-SCHEDULES = {"thread_mapped": 0, "group_mapped": 1, "merge_path": 2, "block_mapped": 3}
+SCHEDULES = {"thread_mapped": 0, "group_mapped": 1, "merge_path": 2, "block_mapped": 3, "auto": 4}
+SCHEDULE_NAMES = {v: k for k, v in SCHEDULES.items()}
 LB_SPMV_REPARTITION = 1
 DEFAULT_ITEMS_PER_TILE = 1016
 TILE_LENGTHS = (504, 1016, 2040, 3064, 4088)
@@ -74,6 +75,7 @@ def lib() -> ctypes.CDLL:
         "lb_spmv_multi": ([p, p, ctypes.c_int, p, p, p, p], st),
         "lb_allgather_rows": ([p, p, p, p], st),
         "lb_kernel_name": ([p, ctypes.c_int], ctypes.c_char_p),
+        "lb_select_schedule": ([p, p, ctypes.POINTER(ctypes.c_int)], st),
         "lb_last_error": ([], ctypes.c_char_p),
         "lb_launch_count": ([], ctypes.c_uint64),
         "lb_version": ([], ctypes.c_char_p),
@@ -151,7 +153,7 @@ class CsrMatrix:
                                        self.values.data_ptr() if self.nnz else None, int(bool(validate)),
                                        _stream(stream), ctypes.byref(self._h)))
         self.device = self.row_offsets.device
-        self.items_per_tile = DEFAULT_ITEMS_PER_TILE
+        self.items_per_tile = 2040 if self.nnz < 8 * self.rows else DEFAULT_ITEMS_PER_TILE
 
     @classmethod
     def from_csr(cls, A, device="cuda", validate: bool = True) -> "CsrMatrix":
@@ -178,7 +180,7 @@ class CsrMatrix:
 
     def set_items_per_tile(self, L: int):
         _check(lib().lb_csr_set_items_per_tile(self.handle, int(L)))
-        self.items_per_tile = int(L) or DEFAULT_ITEMS_PER_TILE
+        self.items_per_tile = int(L) or (2040 if self.nnz < 8 * self.rows else DEFAULT_ITEMS_PER_TILE)
 
     def num_tiles(self, items_per_tile: int = 0) -> int:
         n = ctypes.c_int64()
@@ -205,6 +207,12 @@ class CsrMatrix:
         _check(lib().lb_spmv_ex(self.handle, _sched(schedule), x.data_ptr() if self.cols else None,
                                 y.data_ptr() if self.rows else None, flags, _stream(stream)))
         return y
+
+    def select_schedule(self, stream=None) -> str:
+        """The schedule LB_SCHED_AUTO resolves to for this matrix (lb_select_schedule)."""
+        out = ctypes.c_int()
+        _check(lib().lb_select_schedule(self.handle, _stream(stream), ctypes.byref(out)))
+        return SCHEDULE_NAMES[out.value]
 
     def kernel_name(self, schedule="merge_path") -> str:
         """Main kernel lb_spmv launches for `schedule` (lb_kernel_name)."""

@@ -20,7 +20,7 @@ import paper_2212_08964_b200 as lb
 
 pytestmark = pytest.mark.gpu
 
-SCHEDS = ["merge_path", "thread_mapped", "group_mapped", "block_mapped"]
+SCHEDS = ["merge_path", "thread_mapped", "group_mapped", "block_mapped", "auto"]
 TOL = 1e-5
 
 
@@ -373,7 +373,8 @@ def test_full_size_configs(cfg):
 
 
 # ---------------------------------------------------------------- every tile-kernel variant
-VARIANTS = [(0, 1016), (1, 2040), (2, 4088), (3, 504), (4, 3064), (5, 1016), (6, 1016), (7, 504), (8, 504)]
+VARIANTS = [(0, 1016), (1, 2040), (2, 4088), (3, 504), (4, 3064), (5, 1016), (6, 1016), (7, 504), (8, 504),
+            (9, 1016), (10, 1016), (11, 2040), (12, 504)]
 
 
 @pytest.mark.parametrize("variant,L", VARIANTS)
@@ -395,3 +396,20 @@ def test_every_merge_variant(variant, L, monkeypatch):
         x = torch.ones(A.cols)
         y_ref, s_ref = ref(A, x)
         check_y(run(A, x, "merge_path", L), y_ref, s_ref, True, f"v{variant}/{name}")
+
+
+# ---------------------------------------------------------------- AUTO schedule (P:1149 + reading R18)
+
+def test_auto_schedule_selection_and_parity():
+    cases = {
+        "tiny (alpha/beta rule)": (_csr(list(range(0, 401)), 300), "thread_mapped"),
+        "stencil (regular rows)": (lbgen.stencil(120, 2, "int"), "thread_mapped"),
+        "rmat (power law)": (lbgen.rmat(13, 16, 5, "int"), "merge_path"),
+        "skewed (giant rows)": (lbgen.skewed(1 << 12, 3, 30_000, 20_000, 8, "int"), "merge_path"),
+    }
+    for name, (A, want) in cases.items():
+        M = lb.CsrMatrix.from_csr(A)
+        assert M.select_schedule() == want, name
+        x = lbgen.make_x(A.cols, "int", 2)
+        y_ref, s_ref = ref(A, x)
+        check_y(M.spmv(x.cuda(), schedule="auto"), y_ref, s_ref, True, name)
