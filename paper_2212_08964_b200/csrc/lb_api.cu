@@ -125,9 +125,9 @@ template <int NT, int E, int MINB>
 lb_status_t wide_launch(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s);
 #define LB_WIDE_VARIANT(NT, E, MINB) {NT * E - 8, NT, E, MINB, 2, wide_prepare<NT, E, MINB>, wide_launch<NT, E, MINB>}
 
-template <int W, int R, int MINB>
+template <int W, int R, int MINB, bool XK>
 lb_status_t stream_prepare(int* blocks) {
-  auto k = lbk::merge_stream_kernel<W, R, MINB>;
+  auto k = lbk::merge_stream_kernel<W, R, MINB, XK>;
   cudaFuncAttributes fa;
   LB_CUDA(cudaFuncGetAttributes(&fa, k));
   LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k, W * 32, 0));
@@ -138,11 +138,13 @@ lb_status_t stream_prepare(int* blocks) {
   LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, k, W * 32, 0));
   return LB_OK;
 }
-template <int W, int R, int MINB>
+template <int W, int R, int MINB, bool XK>
 lb_status_t stream_launch(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s);
 // warp-streamed tiles: L = 256*R - 8, W warps per CTA (nt = W*32, e = 8 nonzeros per lane per round)
 #define LB_STREAM_VARIANT(W, R, MINB) \
-  {256 * R - 8, W * 32, 8, MINB, 3, stream_prepare<W, R, MINB>, stream_launch<W, R, MINB>}
+  {256 * R - 8, W * 32, 8, MINB, 3, stream_prepare<W, R, MINB, false>, stream_launch<W, R, MINB, false>}
+#define LB_STREAM_VARIANT_XK(W, R, MINB) \
+  {256 * R - 8, W * 32, 8, MINB, 3, stream_prepare<W, R, MINB, true>, stream_launch<W, R, MINB, true>}
 
 #define LB_DIRECT_VARIANT(NT, MINB, XK) \
   {NT * 4 - 8, NT, 4, MINB, 0, direct_prepare<NT, MINB, XK>, direct_launch<NT, MINB, XK>}
@@ -161,6 +163,7 @@ const PipeVariant kVariants[] = {
     LB_STREAM_VARIANT(4, 4, 4),        // 10 L=1016 alternative: warp-streamed, 4 warps/CTA
     LB_STREAM_VARIANT(4, 8, 4),        // 11 L=2040 alternative: warp-streamed
     LB_WIDE_VARIANT(64, 8, 16),        // 12 L=504  alternative
+    LB_STREAM_VARIANT_XK(8, 4, 2),     // 13 L=1016 warp-streamed, x gathers with L2 evict_last
 };
 constexpr int kNumVariants = sizeof(kVariants) / sizeof(kVariants[0]);
 // default variant per tile length (index into kVariants), chosen by measurement
@@ -431,7 +434,7 @@ lb_status_t wide_launch(lb_csr_s* A, const float* x, float* y, int grid_max, str
   return LB_OK;
 }
 
-template <int W, int R, int MINB>
+template <int W, int R, int MINB, bool XK>
 lb_status_t stream_launch(lb_csr_s* A, const float* x, float* y, int grid_max, stream_t s) {
   constexpr int L = 256 * R - 8;
   const int T = (int)num_tiles(A->rows, A->nnz, L);
@@ -454,7 +457,7 @@ lb_status_t stream_launch(lb_csr_s* A, const float* x, float* y, int grid_max, s
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  LB_CUDA(cudaLaunchKernelEx(&cfg, lbk::merge_stream_kernel<W, R, MINB>, a));
+  LB_CUDA(cudaLaunchKernelEx(&cfg, lbk::merge_stream_kernel<W, R, MINB, XK>, a));
   LB_LAUNCHED();
   return LB_OK;
 }

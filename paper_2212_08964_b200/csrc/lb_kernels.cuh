@@ -1026,17 +1026,18 @@ __device__ __forceinline__ void stream_load(const PipeArgs& a, int4 c, int k, in
 }
 
 // gathers x for the round's valid positions; invalid positions get val = 0 (they add exactly 0)
+template <bool XKEEP>
 __device__ __forceinline__ void stream_gather(const PipeArgs& a, int4 c, int k, int lane, StreamRound& d,
-                                              float (&xv)[8]) {
+                                              float (&xv)[8], uint64_t xpol) {
   const int q0 = 256 * k + 8 * lane, lo = c.y & 7, hi = c.w - (c.y & ~7);
   if (q0 >= lo && q0 + 8 <= hi) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) xv[e] = ld_x(a.x + d.col[e]);
+    for (int e = 0; e < 8; ++e) xv[e] = XKEEP ? ld_x_keep(a.x + d.col[e], xpol) : ld_x(a.x + d.col[e]);
   } else {
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const bool ok = q0 + e >= lo && q0 + e < hi;
-      xv[e] = ok ? ld_x(a.x + d.col[e]) : 0.f;
+      xv[e] = ok ? (XKEEP ? ld_x_keep(a.x + d.col[e], xpol) : ld_x(a.x + d.col[e])) : 0.f;
       if (!ok) d.val[e] = 0.f;
     }
   }
@@ -1050,8 +1051,8 @@ __device__ __forceinline__ void stream_prefetch_offsets(const PipeArgs& a, int4 
   for (int j = 0; j < K; ++j) {
     const int r = lane + 32 * j;
     if (r < nrows) {
-      lo_[j] = __ldg(a.off + c.x + r);
-      hi_[j] = __ldg(a.off + c.x + r + 1);
+      lo_[j] = __ldcs(a.off + c.x + r);
+      hi_[j] = __ldcs(a.off + c.x + r + 1);
     }
   }
 }
@@ -1073,20 +1074,20 @@ __device__ __forceinline__ bool stream_row_pass(const PipeArgs& a, int4 c, int l
         for (int q = 0; q < K; ++q)
           if (q == j) { ob = lo_[q]; oe = hi_[q]; }
       } else {
-        ob = __ldg(a.off + i0 + r);
-        oe = __ldg(a.off + i0 + r + 1);
+        ob = __ldcs(a.off + i0 + r);
+        oe = __ldcs(a.off + i0 + r + 1);
       }
       const int e = oe - jA;
       const int s = r == 0 ? lo : ob - jA;
       if (e > s) tail[e - 1] = (unsigned short)(r + 1);
-      else if (r > 0) a.y[i0 + r] = 0.f;
+      else if (r > 0) __stcs(a.y + i0 + r, 0.f);
       else row0_empty = true;
     }
   }
   return __shfl_sync(kFull, (int)row0_empty, 0) != 0;
 }
 
-template <int W, int R, int MINB>
+template <int W, int R, int MINB, bool XKEEP>
 __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) {
   using Cfg = StreamCfg<R>;
   constexpr int K = Cfg::K;
@@ -1098,6 +1099,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
   const int t_begin = min(a.num_tiles, gw * a.tiles_per_cta);
   const int t_end = min(a.num_tiles, t_begin + a.tiles_per_cta);
   const uint64_t spol = policy_evict_first();
+  const uint64_t xpol = XKEEP ? policy_evict_last() : 0ull;
   unsigned short* tail = s_tail[warp];
   for (int w = lane; w < Cfg::kCap / 8; w += 32) reinterpret_cast<uint4*>(tail)[w] = make_uint4(0u, 0u, 0u, 0u);
   asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: coords are read below
@@ -1121,14 +1123,14 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
     float x0[8], x1[8];
     stream_load(a, cT, 0, lane, d0, spol);
     if (1 < nsteps) stream_load(a, R > 1 ? cT : cT1, R > 1 ? 1 : 0, lane, d1, spol);
-    stream_gather(a, cT, 0, lane, d0, x0);
+    stream_gather<XKEEP>(a, cT, 0, lane, d0, x0, xpol);
 
     int t = t_begin, k = 0;
     for (int st = 0; st < nsteps; ++st) {
       // (a) gathers for step st+1, loads for step st+2
       if (st + 1 < nsteps) {
         const bool same = k + 1 < R;
-        stream_gather(a, same ? cT : cT1, same ? k + 1 : k + 1 - R, lane, d1, x1);
+        stream_gather<XKEEP>(a, same ? cT : cT1, same ? k + 1 : k + 1 - R, lane, d1, x1, xpol);
       }
       if (st + 2 < nsteps) {
         const int k2 = k + 2;
@@ -1138,7 +1140,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
       // (b) the row open at the tile start has no nonzero here: it ends now with the carry
       const int i0 = cT.x;
       if (k == 0 && r0e) {
-        if (lane == 0) a.y[i0] = rc;
+        if (lane == 0) __stcs(a.y + i0, rc);
         rc = 0.f;
       }
       // (c) reduce this round
@@ -1153,7 +1155,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
         if (rid) {
           const int r = (int)rid - 1;
           if (first_r < 0) { first_r = r; first_val = run; }
-          else a.y[i0 + r] = run;  // row started inside this lane's 8 nonzeros
+          else __stcs(a.y + i0 + r, run);  // row started inside this lane's 8 nonzeros
           run = 0.f;
         }
       }
@@ -1166,7 +1168,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
       const float agg_v = __shfl_sync(kFull, v, 31);
       if (first_r >= 0) {
         const float carry_in = lane == 0 ? rc : (lf ? lval : rc + lval);
-        a.y[i0 + first_r] = carry_in + first_val;
+        __stcs(a.y + i0 + first_r, carry_in + first_val);
       }
       if (tr[0] | tr[1] | tr[2] | tr[3])
         *reinterpret_cast<uint4*>(&tail[256 * k + 8 * lane]) = make_uint4(0u, 0u, 0u, 0u);

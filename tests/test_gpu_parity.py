@@ -374,7 +374,7 @@ def test_full_size_configs(cfg):
 
 # ---------------------------------------------------------------- every tile-kernel variant
 VARIANTS = [(0, 1016), (1, 2040), (2, 4088), (3, 504), (4, 3064), (5, 1016), (6, 1016), (7, 504), (8, 504),
-            (9, 1016), (10, 1016), (11, 2040), (12, 504)]
+            (9, 1016), (10, 1016), (11, 2040), (12, 504), (13, 1016)]
 
 
 @pytest.mark.parametrize("variant,L", VARIANTS)

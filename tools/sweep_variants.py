@@ -5,7 +5,7 @@ import numpy as np, torch
 import lbgen, oracle
 import paper_2212_08964_b200 as lb
 
-VARIANTS = [(0, 1016), (1, 2040), (9, 1016), (10, 1016), (11, 1016), (12, 504), (13, 2040), (14, 1016)]
+VARIANTS = [(0, 1016), (13, 1016), (10, 1016), (3, 504), (11, 2040)]
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c3"
 # correctness on a small int matrix
 As = lbgen.rmat(13, 16, 5, "int"); xs = lbgen.make_x(As.cols, "int", 3)
