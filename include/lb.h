@@ -148,6 +148,16 @@ lb_status_t lb_spmv(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_
  * and caches the row statistics on first use: one reduction kernel + one sync of `stream`). */
 lb_status_t lb_select_schedule(lb_csr_t A, void* stream, lb_schedule_t* out);
 
+/*
+ * lb_spmm -- Y = A X for a dense X with n columns (Listing 4: SpMM is SpMV with a loop
+ * over the columns of B), on the same merge-path tiles (L = 1016; lb_partition's output at that
+ * length is reused).  X: fp32 [cols x n] row-major with leading dimension ldx >= n; Y: fp32
+ * [rows x n], leading dimension ldy >= n, overwritten.  Columns are processed in panels of 4 (one
+ * 16-byte gather of X[col, c..c+4) per nonzero) when X, Y are 16-byte aligned and ldx, ldy are
+ * multiples of 4, otherwise one column at a time.  X and Y must not alias.
+ */
+lb_status_t lb_spmm(lb_csr_t A, int64_t n, const float* d_X, int64_t ldx, float* d_Y, int64_t ldy, void* stream);
+
 /* Flags for lb_spmv_ex. */
 #define LB_SPMV_REPARTITION 1u /* MERGE_PATH: recompute the partition inside this call */
 

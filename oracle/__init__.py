@@ -40,6 +40,7 @@ def lib():
         L.oracle_spmv.argtypes = [i64, p, p, p, p, p, p]
         L.oracle_spmv_omp.argtypes = [i64, p, p, p, p, p, p]
         L.oracle_spmv_packed.argtypes = [i64, p, p, p, p, p, p]
+        L.oracle_spmm.argtypes = [i64, p, p, p, i64, p, i64, p, i64, p]
         L.oracle_partition.argtypes = [i64, i64, p, i64, p]
         L.oracle_partition.restype = i64
         L.oracle_shard_bounds.argtypes = [i64, p, ctypes.c_int32, p]
@@ -72,6 +73,20 @@ def spmv(row_offsets, col_idx, values, x, threads: bool = False):
     f = lib().oracle_spmv_omp if threads else lib().oracle_spmv
     f(rows, _ptr(off), _ptr(col), _ptr(val), _ptr(xx), _ptr(y), _ptr(s))
     return y, s
+
+
+def spmm(row_offsets, col_idx, values, X):
+    """Y = A X in double (X: [cols, n] row-major), plus S = sum |a_ik X_kj|.  Returns (Y, S)."""
+    off = _np(row_offsets, np.int32)
+    col = _np(col_idx, np.int32)
+    val = _np(values, np.float32)
+    XX = _np(X, np.float32)
+    rows = off.size - 1
+    n = XX.shape[1] if XX.ndim == 2 else 1
+    Y = np.empty((rows, n), np.float64)
+    S = np.empty((rows, n), np.float64)
+    lib().oracle_spmm(rows, _ptr(off), _ptr(col), _ptr(val), n, _ptr(XX), n, _ptr(Y), n, _ptr(S))
+    return Y, S
 
 
 def spmv_packed(sel_offsets, sel_cols, sel_vals, x):

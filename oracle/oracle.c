@@ -93,6 +93,29 @@ void oracle_spmv_packed(int64_t n_sel, const int64_t *sel_offsets, const int32_t
 }
 
 /*
+ * SpMM by definition: Y = A X for A in CSR and X dense, row-major with leading dimension ldx
+ * (Listing 4 P:1046-1074 [Sec. Application Space]: "a simple loop wrapped around SpMV": for each
+ * row and each column j of X, sum += values[nz] * X(indices[nz], j); C(row, j) = sum).
+ * Y[i*ldy + j] = sum_k val[k] * X[col[k]*ldx + j] in row order, in double; S likewise with |.|.
+ */
+void oracle_spmm(int64_t rows, const int32_t *row_offsets, const int32_t *col_idx, const float *values,
+                 int64_t n, const float *X, int64_t ldx, double *Y, int64_t ldy, double *S)
+{
+    for (int64_t i = 0; i < rows; ++i) {
+        for (int64_t j = 0; j < n; ++j) {
+            double acc = 0.0, mag = 0.0;
+            for (int64_t k = row_offsets[i]; k < row_offsets[i + 1]; ++k) {
+                double p = (double)values[k] * (double)X[(int64_t)col_idx[k] * ldx + j];
+                acc += p;
+                mag += fabs(p);
+            }
+            Y[i * ldy + j] = acc;
+            if (S) S[i * ldy + j] = mag;
+        }
+    }
+}
+
+/*
  * Merge-path partition by brute force: walk the merge of list A = the row ends
  * (row i ends after its off[i+1] nonzeros) and list B = the nonzero indices 0..nnz-1,
  * one merge item per step, exactly as the merge-path schedule defines the work

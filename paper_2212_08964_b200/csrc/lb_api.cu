@@ -245,6 +245,7 @@ struct lb_csr_s {
   bool vec32 = true;          // col/val 32-byte aligned -> 256-bit loads (wide tile kernel)
   int L = LB_DEFAULT_ITEMS_PER_TILE;
   bool coords_valid = false;
+  int coords_L = 0;           // tile length the cached partition was computed for
   bool owns_scratch = true;
   int2* coords = nullptr;     // partition cache [(T_max+1)]
   int* carry_row = nullptr;   // [kMaxCtas]
@@ -262,7 +263,7 @@ size_t align256(size_t n) { return (n + 255) & ~size_t(255); }
 
 size_t scratch_bytes(int64_t rows, int64_t nnz) {
   return align256((num_tiles(rows, nnz, kMinTile) + 1) * sizeof(int2)) + align256(kMaxCtas * sizeof(int)) +
-         align256(kMaxCtas * sizeof(float)) + align256(4 * sizeof(int)) + align256(sizeof(unsigned));
+         align256(4 * kMaxCtas * sizeof(float)) + align256(4 * sizeof(int)) + align256(sizeof(unsigned));
 }
 
 void carve_scratch(lb_csr_s* A, char* p) {
@@ -271,7 +272,7 @@ void carve_scratch(lb_csr_s* A, char* p) {
   A->carry_row = reinterpret_cast<int*>(p);
   p += align256(kMaxCtas * sizeof(int));
   A->carry_val = reinterpret_cast<float*>(p);
-  p += align256(kMaxCtas * sizeof(float));
+  p += align256(4 * kMaxCtas * sizeof(float));  // up to 4 values per carry (SpMM panels)
   A->flags = reinterpret_cast<int*>(p);
   p += align256(4 * sizeof(int));
   A->ticket = reinterpret_cast<unsigned*>(p);
@@ -543,9 +544,10 @@ lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y
     }
     case LB_SCHED_MERGE_PATH: {
       lb_status_t st;
-      if (!A->coords_valid || (flags & LB_SPMV_REPARTITION)) {
+      if (!A->coords_valid || A->coords_L != A->L || (flags & LB_SPMV_REPARTITION)) {
         if ((st = launch_partition(A, A->L, A->coords, s)) != LB_OK) return st;
         A->coords_valid = true;
+        A->coords_L = A->L;
       }
       if (pe) LB_CUDA(cudaEventRecord(pe->ev[1], s));
       switch (A->L) {
@@ -560,6 +562,63 @@ lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y
     default:
       return fail(LB_ERR_INVALID_ARG, "unknown schedule id %d", (int)sched);
   }
+}
+
+constexpr int kSpmmW = 8, kSpmmMinB = 2, kSpmmL = 1016;
+
+template <int P>
+lb_status_t spmm_panel(lb_csr_s* A, const float* X, int64_t ldx, float* Y, int64_t ldy, stream_t s) {
+  auto k = lbk::merge_spmm_kernel<kSpmmW, P, kSpmmMinB>;
+  static int blocks_cache[64][2] = {{0}};
+  int& blocks = blocks_cache[A->device][P == 4];
+  if (blocks == 0) {
+    cudaFuncAttributes fa;
+    LB_CUDA(cudaFuncGetAttributes(&fa, k));
+    LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, kSpmmW * 32, 0));
+    const double need = (double)blocks * (fa.sharedSizeBytes + 1024);
+    int pct = std::min(100, std::max(1, (int)(100.0 * need / (228.0 * 1024.0)) + 1));
+    LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, kSpmmW * 32, 0));
+    blocks = std::max(1, blocks);
+  }
+  const int T = (int)num_tiles(A->rows, A->nnz, kSpmmL);
+  const int warps_max = std::min(A->dev->sm_count * blocks * kSpmmW, kMaxCtas);
+  const int tpw = (T + warps_max - 1) / warps_max;
+  const int warps = (T + tpw - 1) / tpw;
+  const int grid = (warps + kSpmmW - 1) / kSpmmW;
+  lbk::SpmmArgs a;
+  a.off = A->off; a.col = A->col; a.val = A->val; a.X = X; a.Y = Y; a.ldx = ldx; a.ldy = ldy;
+  a.coords = A->coords; a.rows = (int)A->rows; a.nnz = (int)A->nnz; a.num_tiles = T; a.tiles_per_warp = tpw;
+  a.carry_row = A->carry_row; a.carry_val = A->carry_val; a.ticket = A->ticket; a.vec = A->vec ? 1 : 0;
+  k<<<grid, kSpmmW * 32, 0, s>>>(a);
+  LB_LAUNCHED();
+  return LB_OK;
+}
+
+lb_status_t spmm_impl(lb_csr_s* A, int64_t n, const float* X, int64_t ldx, float* Y, int64_t ldy, stream_t s) {
+  if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
+  if (n < 0 || ldx < n || ldy < n) return fail(LB_ERR_INVALID_ARG, "need n >= 0, ldx >= n, ldy >= n");
+  if (A->rows == 0 || n == 0) return LB_OK;
+  if (!Y || (!X && A->nnz > 0)) return fail(LB_ERR_INVALID_ARG, "null X or Y");
+  if ((const void*)X == (const void*)Y) return fail(LB_ERR_INVALID_ARG, "X and Y must not alias");
+  lb_status_t st;
+  if (!A->coords_valid || A->coords_L != kSpmmL) {
+    if ((st = launch_partition(A, kSpmmL, A->coords, s)) != LB_OK) return st;
+    A->coords_valid = true;
+    A->coords_L = kSpmmL;
+  }
+  for (int64_t c0 = 0; c0 < n;) {
+    const bool quad = n - c0 >= 4 && ldx % 4 == 0 && ldy % 4 == 0 &&
+                      reinterpret_cast<uintptr_t>(X + c0) % 16 == 0 && reinterpret_cast<uintptr_t>(Y + c0) % 16 == 0;
+    if (quad) {
+      if ((st = spmm_panel<4>(A, X + c0, ldx, Y + c0, ldy, s)) != LB_OK) return st;
+      c0 += 4;
+    } else {
+      if ((st = spmm_panel<1>(A, X + c0, ldx, Y + c0, ldy, s)) != LB_OK) return st;
+      c0 += 1;
+    }
+  }
+  return LB_OK;
 }
 
 }  // namespace
@@ -663,6 +722,11 @@ lb_status_t lb_partition(lb_csr_t A, int32_t items_per_tile, int32_t* d_coords, 
 lb_status_t lb_spmv(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_y, void* stream) {
   g_err.clear();
   return spmv_impl(A, sched, d_x, d_y, 0u, S(stream), nullptr);
+}
+
+lb_status_t lb_spmm(lb_csr_t A, int64_t n, const float* d_X, int64_t ldx, float* d_Y, int64_t ldy, void* stream) {
+  g_err.clear();
+  return spmm_impl(A, n, d_X, ldx, d_Y, ldy, S(stream));
 }
 
 lb_status_t lb_spmv_ex(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_y, uint32_t flags, void* stream) {

@@ -1220,6 +1220,293 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
   }
 }
 
+// ----------------------------------------------------------------------------- SpMM (NEXT-2)
+// Y = A X for a panel of P (1 or 4) columns of a row-major X (Listing 4: "a simple loop
+// wrapped around SpMV"), on the same merge-path tiles as SpMV (L = 1016, lb_partition's output is
+// reused).  Warp-streamed like merge_stream_kernel, with 4 nonzeros per lane per round (128 per
+// warp-round, 8 rounds per tile) and one P-wide gather X[col, c0 .. c0+P) per nonzero: with P = 4
+// a single 16-byte gather feeds 4 outputs, which is what lifts SpMM above SpMV's gather bound.
+struct SpmmArgs {
+  const int* off;
+  const int* col;
+  const float* val;
+  const float* X;  // panel base: &X[0, c0]
+  float* Y;        // panel base: &Y[0, c0]
+  int64_t ldx, ldy;
+  const int2* coords;
+  int rows, nnz;
+  int num_tiles;
+  int tiles_per_warp;
+  int* carry_row;
+  float* carry_val;  // [warps * P]
+  unsigned* ticket;
+  int vec;           // col/val 16-byte aligned -> 128-bit loads
+};
+
+template <int P>
+struct PVec;
+template <>
+struct PVec<1> {
+  float v[1];
+};
+template <>
+struct PVec<4> {
+  float v[4];
+};
+
+template <int P>
+__device__ __forceinline__ void spmm_gather(const SpmmArgs& a, int c, PVec<P>& out) {
+  const float* src = a.X + (int64_t)c * a.ldx;
+  if (P == 4) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(src));
+    out.v[0] = t.x; out.v[1] = t.y; out.v[2] = t.z; out.v[3] = t.w;
+  } else {
+    out.v[0] = __ldg(src);
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void spmm_store(const SpmmArgs& a, int row, const float (&v)[P]) {
+  float* dst = a.Y + (int64_t)row * a.ldy;
+  if (P == 4) __stcs(reinterpret_cast<float4*>(dst), make_float4(v[0], v[1], v[2], v[3]));
+  else __stcs(dst, v[0]);
+}
+
+struct SpmmRound {
+  int col[4];
+  float val[4];
+};
+
+__device__ __forceinline__ void spmm_load(const SpmmArgs& a, int4 c, int k, int lane, SpmmRound& d) {
+  const int g = (c.y & ~7) + 128 * k + 4 * lane;
+  if (a.vec && g < c.w && g + 4 <= a.nnz) {
+    const int4 ci = ld_cs_v4(a.col + g);
+    const float4 vi = ld_cs_v4(a.val + g);
+    d.col[0] = ci.x; d.col[1] = ci.y; d.col[2] = ci.z; d.col[3] = ci.w;
+    d.val[0] = vi.x; d.val[1] = vi.y; d.val[2] = vi.z; d.val[3] = vi.w;
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const bool ok = g + e < c.w;
+      d.col[e] = ok ? ld_cs(a.col + g + e) : 0;
+      d.val[e] = ok ? ld_cs(a.val + g + e) : 0.f;
+    }
+  }
+}
+
+template <int P>
+__device__ __forceinline__ void spmm_gather_round(const SpmmArgs& a, int4 c, int k, int lane, SpmmRound& d,
+                                                  PVec<P> (&xv)[4]) {
+  const int q0 = 128 * k + 4 * lane, lo = c.y & 7, hi = c.w - (c.y & ~7);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const bool ok = q0 + e >= lo && q0 + e < hi;
+    if (ok) spmm_gather<P>(a, d.col[e], xv[e]);
+    else {
+#pragma unroll
+      for (int j = 0; j < P; ++j) xv[e].v[j] = 0.f;
+      d.val[e] = 0.f;
+    }
+  }
+}
+
+template <int W, int P, int MINB>
+__global__ void __launch_bounds__(W * 32, MINB) merge_spmm_kernel(SpmmArgs a) {
+  constexpr int kCap = 1024, R = 8;  // tile positions, rounds of 128 per tile (L = 1016)
+  constexpr int K = 2;
+  __shared__ __align__(16) unsigned short s_tail[W][kCap];
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int gw = blockIdx.x * W + warp;
+  const int t_begin = min(a.num_tiles, gw * a.tiles_per_warp);
+  const int t_end = min(a.num_tiles, t_begin + a.tiles_per_warp);
+  unsigned short* tail = s_tail[warp];
+  for (int w = lane; w < kCap / 8; w += 32) reinterpret_cast<uint4*>(tail)[w] = make_uint4(0u, 0u, 0u, 0u);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __syncwarp();
+
+  // reuse the SpMV row pass (it only reads off/coords and writes y = 0 for empty rows: for SpMM the
+  // empty rows are written here instead, so give it a PipeArgs whose y is unused (nullptr never hit
+  // because we handle empty rows ourselves below)
+  PipeArgs pa;
+  pa.off = a.off; pa.coords = a.coords; pa.rows = a.rows; pa.nnz = a.nnz;
+  float rc[P];
+#pragma unroll
+  for (int j = 0; j < P; ++j) rc[j] = 0.f;
+  int i_last = t_begin < t_end ? __ldg(&a.coords[t_end].x) : a.rows;
+  if (t_begin < t_end) {
+    const int nsteps = (t_end - t_begin) * R;
+    int4 cT = tile_coords(pa, t_begin);
+    int4 cT1 = t_begin + 1 < t_end ? tile_coords(pa, t_begin + 1) : cT;
+    int4 cT2 = t_begin + 2 < t_end ? tile_coords(pa, t_begin + 2) : cT1;
+    int olo[K], ohi[K];
+    // row pass writing empty rows of Y (rows r > 0 without a nonzero in the tile)
+    auto row_pass = [&](int4 c) -> bool {
+      const int i0 = c.x, nrows = c.z - c.x, jA = c.y & ~7, lo = c.y - jA;
+      bool row0_empty = false;
+      for (int j = 0; 32 * j < nrows; ++j) {
+        const int r = lane + 32 * j;
+        if (r < nrows) {
+          int ob, oe;
+          if (j < K) {
+#pragma unroll
+            for (int q = 0; q < K; ++q)
+              if (q == j) { ob = olo[q]; oe = ohi[q]; }
+          } else {
+            ob = __ldcs(a.off + i0 + r);
+            oe = __ldcs(a.off + i0 + r + 1);
+          }
+          const int e = oe - jA;
+          const int s = r == 0 ? lo : ob - jA;
+          if (e > s) tail[e - 1] = (unsigned short)(r + 1);
+          else if (r > 0) {
+            float z[P];
+#pragma unroll
+            for (int q = 0; q < P; ++q) z[q] = 0.f;
+            spmm_store<P>(a, i0 + r, z);
+          } else row0_empty = true;
+        }
+      }
+      return __shfl_sync(kFull, (int)row0_empty, 0) != 0;
+    };
+    stream_prefetch_offsets<4, K>(pa, cT, lane, olo, ohi);
+    bool r0e = row_pass(cT);
+    if (t_begin + 1 < t_end) stream_prefetch_offsets<4, K>(pa, cT1, lane, olo, ohi);
+    __syncwarp();
+    SpmmRound d0, d1, d2;
+    PVec<P> x0[4], x1[4];
+    spmm_load(a, cT, 0, lane, d0);
+    if (1 < nsteps) spmm_load(a, cT, 1, lane, d1);
+    spmm_gather_round<P>(a, cT, 0, lane, d0, x0);
+    int t = t_begin, k = 0;
+    for (int st = 0; st < nsteps; ++st) {
+      if (st + 1 < nsteps) {
+        const bool same = k + 1 < R;
+        spmm_gather_round<P>(a, same ? cT : cT1, same ? k + 1 : k + 1 - R, lane, d1, x1);
+      }
+      if (st + 2 < nsteps) {
+        const int k2 = k + 2;
+        const bool same = k2 < R;
+        spmm_load(a, same ? cT : cT1, same ? k2 : k2 - R, lane, d2);
+      }
+      const int i0 = cT.x;
+      if (k == 0 && r0e) {
+        if (lane == 0) spmm_store<P>(a, i0, rc);
+#pragma unroll
+        for (int j = 0; j < P; ++j) rc[j] = 0.f;
+      }
+      const uint2 tq = *reinterpret_cast<const uint2*>(&tail[128 * k + 4 * lane]);
+      const unsigned rid[4] = {tq.x & 0xFFFFu, tq.x >> 16, tq.y & 0xFFFFu, tq.y >> 16};
+      float run[P], first_val[P];
+#pragma unroll
+      for (int j = 0; j < P; ++j) { run[j] = 0.f; first_val[j] = 0.f; }
+      int first_r = -1;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+#pragma unroll
+        for (int j = 0; j < P; ++j) run[j] = fmaf(d0.val[e], x0[e].v[j], run[j]);
+        if (rid[e]) {
+          const int r = (int)rid[e] - 1;
+          if (first_r < 0) {
+            first_r = r;
+#pragma unroll
+            for (int j = 0; j < P; ++j) first_val[j] = run[j];
+          } else {
+            spmm_store<P>(a, i0 + r, run);
+          }
+#pragma unroll
+          for (int j = 0; j < P; ++j) run[j] = 0.f;
+        }
+      }
+      // segmented scan of the P partial sums (one flag, P values)
+      bool f = first_r >= 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int fo = __shfl_up_sync(kFull, (int)f, o);
+        float vo[P];
+#pragma unroll
+        for (int j = 0; j < P; ++j) vo[j] = __shfl_up_sync(kFull, run[j], o);
+        if (lane >= o) {
+          if (!f) {
+#pragma unroll
+            for (int j = 0; j < P; ++j) run[j] = vo[j] + run[j];
+          }
+          f = f || fo;
+        }
+      }
+      const int lf = __shfl_up_sync(kFull, (int)f, 1);
+      const int agg_f = __shfl_sync(kFull, (int)f, 31);
+      float lval[P], agg_v[P];
+#pragma unroll
+      for (int j = 0; j < P; ++j) {
+        lval[j] = __shfl_up_sync(kFull, run[j], 1);
+        agg_v[j] = __shfl_sync(kFull, run[j], 31);
+      }
+      if (first_r >= 0) {
+        float yv[P];
+#pragma unroll
+        for (int j = 0; j < P; ++j) yv[j] = (lane == 0 ? rc[j] : (lf ? lval[j] : rc[j] + lval[j])) + first_val[j];
+        spmm_store<P>(a, i0 + first_r, yv);
+      }
+      if (tq.x | tq.y) *reinterpret_cast<uint2*>(&tail[128 * k + 4 * lane]) = make_uint2(0u, 0u);
+#pragma unroll
+      for (int j = 0; j < P; ++j) rc[j] = agg_f ? agg_v[j] : rc[j] + agg_v[j];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        d0.val[e] = d1.val[e];
+        x0[e] = x1[e];
+        d1.col[e] = d2.col[e];
+        d1.val[e] = d2.val[e];
+      }
+      if (++k == R) {
+        k = 0;
+        ++t;
+        __syncwarp();
+        if (t < t_end) {
+          r0e = row_pass(cT1);
+          if (t + 1 < t_end) stream_prefetch_offsets<4, K>(pa, cT2, lane, olo, ohi);
+          cT = cT1;
+          cT1 = cT2;
+          if (t + 2 < t_end) cT2 = tile_coords(pa, t + 2);
+        }
+      }
+      __syncwarp();
+    }
+  }
+
+  if (lane == 0) {
+    a.carry_row[gw] = i_last;
+#pragma unroll
+    for (int j = 0; j < P; ++j) a.carry_val[(int64_t)gw * P + j] = rc[j];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned done = atomicAdd(a.ticket, 1u);
+    s_last = done == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    const int nc = (int)gridDim.x * W;
+    for (int c = threadIdx.x; c < nc; c += W * 32) {
+      const int r = __ldcg(a.carry_row + c);
+      if (r >= a.rows) continue;
+      if (c > 0 && __ldcg(a.carry_row + c - 1) == r) continue;
+      float sum[P];
+#pragma unroll
+      for (int j = 0; j < P; ++j) sum[j] = 0.f;
+      for (int kk = c; kk < nc && __ldcg(a.carry_row + kk) == r; ++kk)
+#pragma unroll
+        for (int j = 0; j < P; ++j) sum[j] += __ldcg(a.carry_val + (int64_t)kk * P + j);
+      float* dst = a.Y + (int64_t)r * a.ldy;
+#pragma unroll
+      for (int j = 0; j < P; ++j) dst[j] = __ldcg(dst + j) + sum[j];
+    }
+    if (threadIdx.x == 0) *a.ticket = 0u;
+  }
+}
+
 // ----------------------------------------------------------------------------- thread-mapped
 // Listing 3: for row in tiles() (grid-stride, Listing 2), for nz in
 // atoms(row): sum += values[nz] * x[indices[nz]]; y[row] = sum.  Four independent partial

@@ -65,6 +65,7 @@ def lib() -> ctypes.CDLL:
         "lb_partition": ([p, i32, p, p], st),
         "lb_spmv": ([p, ctypes.c_int, p, p, p], st),
         "lb_spmv_ex": ([p, ctypes.c_int, p, p, u32, p], st),
+        "lb_spmm": ([p, i64, p, i64, p, i64, p], st),
         "lb_spmv_host_workspace_size": ([i64, i64, i64], sz),
         "lb_spmv_host": ([i64, i64, i64, p, p, p, p, p, ctypes.c_int, p, sz, p], st),
         "lb_spmv_phase_times": ([p, ctypes.c_int, p, p, p, ctypes.POINTER(ctypes.c_float)], st),
@@ -213,6 +214,21 @@ class CsrMatrix:
         out = ctypes.c_int()
         _check(lib().lb_select_schedule(self.handle, _stream(stream), ctypes.byref(out)))
         return SCHEDULE_NAMES[out.value]
+
+    def spmm(self, X: torch.Tensor, Y: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Y = A X for a dense row-major X [cols, n] (lb_spmm, merge-path tiles)."""
+        if X.dim() != 2 or X.shape[0] != self.cols:
+            raise ValueError(f"X must be [cols={self.cols}, n]")
+        if X.device.type != "cuda" or X.dtype != torch.float32 or X.stride(1) != 1:
+            raise ValueError("X must be a CUDA float32 tensor with unit column stride")
+        n = X.shape[1]
+        if Y is None:
+            Y = torch.empty((self.rows, n), dtype=torch.float32, device=self.device)
+        if Y.shape != (self.rows, n) or Y.dtype != torch.float32 or Y.stride(1) != 1:
+            raise ValueError("Y must be float32 [rows, n] with unit column stride")
+        _check(lib().lb_spmm(self.handle, n, X.data_ptr() if X.numel() else None, max(X.stride(0), n),
+                             Y.data_ptr() if Y.numel() else None, max(Y.stride(0), n), _stream(stream)))
+        return Y
 
     def kernel_name(self, schedule="merge_path") -> str:
         """Main kernel lb_spmv launches for `schedule` (lb_kernel_name)."""

@@ -413,3 +413,66 @@ def test_auto_schedule_selection_and_parity():
         x = lbgen.make_x(A.cols, "int", 2)
         y_ref, s_ref = ref(A, x)
         check_y(M.spmv(x.cuda(), schedule="auto"), y_ref, s_ref, True, name)
+
+
+# ---------------------------------------------------------------- SpMM (NEXT-2)
+
+def check_Y(Y_gpu, Y_ref, S_ref, exact, what=""):
+    Y = Y_gpu.detach().double().cpu().numpy()
+    assert Y.shape == Y_ref.shape
+    if exact:
+        bad = np.argwhere(Y != Y_ref)
+        assert bad.size == 0, f"{what}: {len(bad)} entries differ, first {bad[:3].tolist()}"
+    else:
+        err = np.abs(Y - Y_ref)
+        assert np.all(err <= TOL * S_ref + 1e-30), f"{what}: worst rel {np.max(err / (S_ref + 1e-30)):.3e}"
+
+
+@pytest.mark.parametrize("n", [1, 3, 4, 5, 8, 16])
+@pytest.mark.parametrize("name", ["rmat12", "stencil100", "skewed", "c1"])
+def test_spmm_parity(name, n):
+    for vm in ("int", "float"):
+        A = SMALL[name](vm)
+        X = lbgen.make_x(A.cols * n, vm, 21).reshape(A.cols, n)
+        Y_ref, S_ref = oracle.spmm(A.row_offsets, A.col_idx, A.values, X)
+        M = lb.CsrMatrix.from_csr(A)
+        Y = M.spmm(X.cuda())
+        torch.cuda.synchronize()
+        check_Y(Y, Y_ref, S_ref, vm == "int", f"{name}/n={n}/{vm}")
+
+
+def test_spmm_strided_and_edge_cases():
+    A = lbgen.rmat(11, 16, 4, "int")
+    Xbig = lbgen.make_x(A.cols * 7, "int", 3).reshape(A.cols, 7).cuda()
+    X = Xbig[:, 1:6]                     # ldx = 7, misaligned base: scalar-column path
+    Y_ref, S_ref = oracle.spmm(A.row_offsets, A.col_idx, A.values, X.cpu().contiguous())
+    M = lb.CsrMatrix.from_csr(A)
+    check_Y(M.spmm(X), Y_ref, S_ref, True, "strided")
+    for nm, B in {"giant": _csr([0, 50_001], 1), "no_nnz": _csr([0] * 2001, 3),
+                  "golden": _csr([0, 1, 3, 3, 6], 1)}.items():
+        X = torch.ones(B.cols, 4)
+        Y_ref, S_ref = oracle.spmm(B.row_offsets, B.col_idx, B.values, X)
+        check_Y(lb.CsrMatrix.from_csr(B).spmm(X.cuda()), Y_ref, S_ref, True, nm)
+    # SpMM column j equals SpMV with x = X[:, j] (same tiles, same arithmetic per column)
+    A = lbgen.rmat(12, 16, 8, "float")
+    X = lbgen.make_x(A.cols * 4, "float", 5).reshape(A.cols, 4).cuda()
+    M = lb.CsrMatrix.from_csr(A)
+    Y = M.spmm(X)
+    Y_ref, S_ref = oracle.spmm(A.row_offsets, A.col_idx, A.values, X.cpu())
+    check_Y(Y, Y_ref, S_ref, False, "float n=4")
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_spmm_full_size(cfg):
+    torch.cuda.empty_cache()
+    A = lbgen.make_config(cfg, "int", device="cuda")
+    X = lbgen.make_x(A.cols * 4, "int", 77, device="cuda").reshape(A.cols, 4)
+    M = lb.CsrMatrix.from_csr(A)
+    Y = M.spmm(X)
+    torch.cuda.synchronize()
+    Yh = Y.cpu()
+    for j in range(4):   # column by column through the oracle SpMV (exact in integer mode)
+        y_ref, s_ref = oracle.spmv(A.row_offsets.cpu(), A.col_idx.cpu(), A.values.cpu(), X[:, j].cpu(), threads=True)
+        check_y(Yh[:, j], y_ref, s_ref, True, f"{cfg} col {j}")
+    del M, A, X, Y
+    torch.cuda.empty_cache()

@@ -316,3 +316,29 @@ def test_shard_bounds(G):
         per = off[b[1:]] - off[b[:-1]]
         assert per.sum() == nnz
         assert np.all(per <= -(-nnz // G) + maxrow)
+
+
+# ---------------------------------------------------------------- SpMM (NEXT-2) pins
+
+@pytest.mark.parametrize("n", [1, 3, 4, 8])
+def test_spmm_dense_brute_force(n):
+    """Y = A X equals the dense product (numpy matmul after densifying) exactly."""
+    rng = np.random.default_rng(n)
+    for trial in range(60):
+        rows, cols = int(rng.integers(0, 30)), int(rng.integers(1, 30))
+        A = random_csr(rng, rows, cols, int(rng.integers(0, 15)), 0.3, "float")
+        X = (rng.integers(-(1 << 23), 1 << 23, (cols, n)) * 2.0 ** -23).astype(np.float32)
+        Y, S = oracle.spmm(A.row_offsets, A.col_idx, A.values, X)
+        D = np.zeros((rows, cols))
+        off = A.row_offsets.numpy().astype(np.int64)
+        np.add.at(D, (np.repeat(np.arange(rows), np.diff(off)), A.col_idx.numpy()), A.values.numpy().astype(np.float64))
+        assert np.array_equal(Y, D @ X.astype(np.float64)), trial
+        assert np.all(S >= np.abs(Y))
+
+
+def test_spmm_identity_closed_form():
+    n = 100
+    off = np.arange(n + 1, dtype=np.int32)
+    X = lbgen.make_x(n * 5, "float", 3).numpy().reshape(n, 5)
+    Y, _ = oracle.spmm(off, np.arange(n, dtype=np.int32), np.ones(n, np.float32), X)
+    assert np.array_equal(Y, X.astype(np.float64))

@@ -43,3 +43,21 @@ for cfg in CFGS:
                           "alg_GB/s_cached": round(alg / ms_cached / 1e6, 1)}), flush=True)
     del M, A, x, y
     torch.cuda.empty_cache()
+
+# SpMM panels (n = 4, 8, 16) on the same merge-path tiles
+for cfg in CFGS:
+    if cfg == "c1":
+        continue
+    A = lbgen.make_config(cfg, "float", device="cuda")
+    M = lb.CsrMatrix.from_csr(A)
+    for n in (4, 8, 16):
+        X = lbgen.make_x(A.cols * n, "float", 5, device="cuda").reshape(A.cols, n)
+        Y = torch.empty(A.rows, n, device="cuda")
+        ms = timeit(lambda: M.spmm(X, Y), 10)
+        alg = (n + 3) // 4 * 8 * A.nnz + 4 * (A.rows + 1) + 4 * n * (A.rows + A.cols)
+        print(json.dumps({"config": cfg, "op": "spmm", "n": n, "ms": round(ms, 4),
+                          "Gnnz_cols_per_s": round(A.nnz * n / ms / 1e6, 1),
+                          "alg_GB/s": round(alg / ms / 1e6, 1)}), flush=True)
+        del X, Y
+    del M, A
+    torch.cuda.empty_cache()
