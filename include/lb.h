@@ -65,6 +65,10 @@ typedef enum {
  *                  P:1018-1028 [Sec. Merge-path load balancing]).
  *  BLOCK_MAPPED    GROUP_MAPPED with G = 256 (a CTA) -- the block-mapped instance the paper gets
  *                  "for free" from the group-mapped schedule (table).
+ *  NONZERO_SPLIT   work-oriented with nonzeros as the only work items (table): tiles of
+ *                  1016 nonzeros, each tile's first row found by a 1-D binary search of
+ *                  row_offsets (lb_partition_nz); rows without nonzeros cost no work, so tiles may
+ *                  span arbitrarily many empty rows.  Runs on the merge-path tile processor.
  *  AUTO            the paper's heuristic: merge-path unless (rows < alpha or cols < alpha)
  *                  and nnz < beta (alpha = 500, beta = 10000), then thread-mapped; extended with a
  *                  row-regularity test for B200 (reading R18): thread-mapped when the longest row
@@ -76,7 +80,8 @@ typedef enum {
   LB_SCHED_GROUP_MAPPED = 1,
   LB_SCHED_MERGE_PATH = 2,
   LB_SCHED_BLOCK_MAPPED = 3,
-  LB_SCHED_AUTO = 4
+  LB_SCHED_AUTO = 4,
+  LB_SCHED_NONZERO_SPLIT = 5
 } lb_schedule_t;
 
 
@@ -134,6 +139,14 @@ lb_status_t lb_partition_size(lb_csr_t A, int32_t items_per_tile, int64_t* num_t
  * Bit-exact: integer arithmetic only.
  */
 lb_status_t lb_partition(lb_csr_t A, int32_t items_per_tile, int32_t* d_coords, void* stream);
+
+/*
+ * lb_partition_nz -- nonzero-splitting partition: T = max(1, ceil(nnz / L)) tiles of L
+ * nonzeros (L = items_per_tile >= 1; 0 = 1016); for 0 < t < T writes (i_t, j_t) with
+ * j_t = t*L and i_t = #{ r : off[r+1] <= j_t } (every row ending at or before nonzero j_t), plus
+ * (0, 0) and (rows, nnz).  d_coords: int32[(T+1)*2] device.  Bit-exact.
+ */
+lb_status_t lb_partition_nz(lb_csr_t A, int32_t items_per_tile, int32_t* d_coords, void* stream);
 
 /*
  * lb_spmv -- y = A x under schedule `sched` (Listing 3; Alg.3).

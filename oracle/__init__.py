@@ -43,6 +43,8 @@ def lib():
         L.oracle_spmm.argtypes = [i64, p, p, p, i64, p, i64, p, i64, p]
         L.oracle_partition.argtypes = [i64, i64, p, i64, p]
         L.oracle_partition.restype = i64
+        L.oracle_partition_nz.argtypes = [i64, i64, p, i64, p]
+        L.oracle_partition_nz.restype = i64
         L.oracle_shard_bounds.argtypes = [i64, p, ctypes.c_int32, p]
         L.oracle_num_threads.restype = ctypes.c_int
         _lib = L
@@ -111,6 +113,18 @@ def partition(row_offsets, L: int) -> np.ndarray:
     out = np.empty((T + 1, 2), np.int32)
     got = lib().oracle_partition(rows, nnz, _ptr(off), L, _ptr(out))
     if got != T:
+        raise ValueError("bad partition arguments")
+    return out
+
+
+def partition_nz(row_offsets, L: int) -> np.ndarray:
+    """Nonzero-splitting tile coordinates (brute force): int32 [T+1, 2] of (row, nz)."""
+    off = _np(row_offsets, np.int32)
+    rows = off.size - 1
+    nnz = int(off[-1]) if rows > 0 else 0
+    T = max(1, (nnz + L - 1) // L)
+    out = np.empty((T + 1, 2), np.int32)
+    if lib().oracle_partition_nz(rows, nnz, _ptr(off), L, _ptr(out)) != T:
         raise ValueError("bad partition arguments")
     return out
 

@@ -154,6 +154,33 @@ int64_t oracle_partition(int64_t rows, int64_t nnz, const int32_t *row_offsets, 
 }
 
 /*
+ * Nonzero-splitting partition (P:291 [Sec. Work-Oriented]: "non-zero splitting ... considers the
+ * total number of nonzero elements ... as the total work"; table): tiles of L nonzeros,
+ * T = max(1, ceil(nnz/L)), j_t = min(t*L, nnz); the tile starts after every row whose end lies at
+ * or before nonzero j_t: i_t = #{ r : off[r+1] <= j_t } (reading R1: a row end precedes the nonzero
+ * at the same position), with i_0 = 0 and i_T = rows so that every row is covered.  By brute force
+ * (linear count).  coords receives (T+1) (row, nz) pairs; returns T.
+ */
+int64_t oracle_partition_nz(int64_t rows, int64_t nnz, const int32_t *row_offsets, int64_t L, int32_t *coords)
+{
+    if (L <= 0 || rows < 0 || nnz < 0) return -1;
+    int64_t T = (nnz + L - 1) / L;
+    if (T < 1) T = 1;
+    for (int64_t t = 0; t <= T; ++t) {
+        int64_t j = t * L < nnz ? t * L : nnz;
+        int64_t i = 0;
+        if (t == 0) i = 0;
+        else if (t == T) i = rows;
+        else
+            for (int64_t r = 0; r < rows; ++r)
+                if (row_offsets[r + 1] <= j) ++i;
+        coords[2 * t] = (int32_t)i;
+        coords[2 * t + 1] = (int32_t)j;
+    }
+    return T;
+}
+
+/*
  * Row-shard bounds for G ranks by equal nnz (reading R9; the paper has no
  * multi-GPU design, P:784 / P:2187-2192): b_0 = 0, b_G = rows, and for 0 < g < G,
  * b_g = min{ r : off[r] >= ceil(g * nnz / G) }, found by a linear scan.

@@ -246,6 +246,7 @@ struct lb_csr_s {
   int L = LB_DEFAULT_ITEMS_PER_TILE;
   bool coords_valid = false;
   int coords_L = 0;           // tile length the cached partition was computed for
+  int coords_kind = 0;        // 0: merge-path, 1: nonzero-split
   bool owns_scratch = true;
   int2* coords = nullptr;     // partition cache [(T_max+1)]
   int* carry_row = nullptr;   // [kMaxCtas]
@@ -336,6 +337,16 @@ lb_status_t launch_partition(const lb_csr_s* A, int64_t L, int2* coords, stream_
 struct PhaseEvents {
   cudaEvent_t ev[4];
 };
+
+int64_t num_tiles_nz(int64_t nnz, int64_t L) { return std::max<int64_t>(1, (nnz + L - 1) / L); }
+
+lb_status_t launch_partition_nz(const lb_csr_s* A, int64_t L, int2* coords, stream_t s) {
+  const int64_t T = num_tiles_nz(A->nnz, L);
+  const int grid = (int)((T + 1 + kNT - 1) / kNT);
+  lbk::partition_nz_kernel<<<grid, kNT, 0, s>>>((int)A->rows, (int)A->nnz, A->off, L, T, coords);
+  LB_LAUNCHED();
+  return LB_OK;
+}
 
 template <int L, bool VEC>
 lb_status_t launch_merge_tiles(lb_csr_s* A, const float* x, float* y, int grid_max, int* grid_used, stream_t s) {
@@ -463,6 +474,38 @@ lb_status_t stream_launch(lb_csr_s* A, const float* x, float* y, int grid_max, s
   return LB_OK;
 }
 
+// nonzero-split: tiles of kNzL nonzeros on the warp-streamed processor with 32-bit row ids
+constexpr int kNzL = 1016;
+lb_status_t launch_nz_tiles(lb_csr_s* A, const float* x, float* y, stream_t s) {
+  constexpr int W = 8, R = 4, MINB = 2;
+  auto k = lbk::merge_stream_kernel<W, R, MINB, false, unsigned>;
+  static int blocks_cache[64] = {0};
+  int& blocks = blocks_cache[A->device];
+  if (blocks == 0) {
+    cudaFuncAttributes fa;
+    LB_CUDA(cudaFuncGetAttributes(&fa, k));
+    LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, W * 32, 0));
+    const double need = (double)blocks * (fa.sharedSizeBytes + 1024);
+    int pct = std::min(100, std::max(1, (int)(100.0 * need / (228.0 * 1024.0)) + 1));
+    LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, W * 32, 0));
+    blocks = std::max(1, blocks);
+  }
+  const int T = (int)num_tiles_nz(A->nnz, kNzL);
+  const int warps_max = std::min(A->dev->sm_count * blocks * W, kMaxCtas);
+  const int tpw = (T + warps_max - 1) / warps_max;
+  const int warps = (T + tpw - 1) / tpw;
+  const int grid = (warps + W - 1) / W;
+  lbk::PipeArgs a;
+  a.off = A->off; a.col = A->col; a.val = A->val; a.x = x; a.y = y;
+  a.coords = A->coords; a.rows = (int)A->rows; a.nnz = (int)A->nnz;
+  a.num_tiles = T; a.tiles_per_cta = tpw;
+  a.carry_row = A->carry_row; a.carry_val = A->carry_val; a.ticket = A->ticket;
+  k<<<grid, W * 32, 0, s>>>(a);
+  LB_LAUNCHED();
+  return LB_OK;
+}
+
 template <int L>
 lb_status_t launch_merge(lb_csr_s* A, const float* x, float* y, stream_t s, PhaseEvents* pe) {
   const int li = l_index(L);
@@ -544,10 +587,11 @@ lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y
     }
     case LB_SCHED_MERGE_PATH: {
       lb_status_t st;
-      if (!A->coords_valid || A->coords_L != A->L || (flags & LB_SPMV_REPARTITION)) {
+      if (!A->coords_valid || A->coords_kind != 0 || A->coords_L != A->L || (flags & LB_SPMV_REPARTITION)) {
         if ((st = launch_partition(A, A->L, A->coords, s)) != LB_OK) return st;
         A->coords_valid = true;
         A->coords_L = A->L;
+        A->coords_kind = 0;
       }
       if (pe) LB_CUDA(cudaEventRecord(pe->ev[1], s));
       switch (A->L) {
@@ -558,6 +602,20 @@ lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y
         case 4088: return launch_merge<4088>(A, x, y, s, pe);
         default: return fail(LB_ERR_INVALID_ARG, "unsupported tile length %d", A->L);
       }
+    }
+    case LB_SCHED_NONZERO_SPLIT: {
+      if (!A->vec32) return fail(LB_ERR_UNSUPPORTED, "nonzero-split needs 32-byte aligned col_idx/values");
+      lb_status_t st;
+      if (!A->coords_valid || A->coords_kind != 1 || A->coords_L != kNzL || (flags & LB_SPMV_REPARTITION)) {
+        if ((st = launch_partition_nz(A, kNzL, A->coords, s)) != LB_OK) return st;
+        A->coords_valid = true;
+        A->coords_L = kNzL;
+        A->coords_kind = 1;
+      }
+      if (pe) LB_CUDA(cudaEventRecord(pe->ev[1], s));
+      if ((st = launch_nz_tiles(A, x, y, s)) != LB_OK) return st;
+      if (pe) { LB_CUDA(cudaEventRecord(pe->ev[2], s)); LB_CUDA(cudaEventRecord(pe->ev[3], s)); }
+      return LB_OK;
     }
     default:
       return fail(LB_ERR_INVALID_ARG, "unknown schedule id %d", (int)sched);
@@ -602,10 +660,11 @@ lb_status_t spmm_impl(lb_csr_s* A, int64_t n, const float* X, int64_t ldx, float
   if (!Y || (!X && A->nnz > 0)) return fail(LB_ERR_INVALID_ARG, "null X or Y");
   if ((const void*)X == (const void*)Y) return fail(LB_ERR_INVALID_ARG, "X and Y must not alias");
   lb_status_t st;
-  if (!A->coords_valid || A->coords_L != kSpmmL) {
+  if (!A->coords_valid || A->coords_kind != 0 || A->coords_L != kSpmmL) {
     if ((st = launch_partition(A, kSpmmL, A->coords, s)) != LB_OK) return st;
     A->coords_valid = true;
     A->coords_L = kSpmmL;
+    A->coords_kind = 0;
   }
   for (int64_t c0 = 0; c0 < n;) {
     const bool quad = n - c0 >= 4 && ldx % 4 == 0 && ldy % 4 == 0 &&
@@ -641,6 +700,7 @@ const char* lb_kernel_name(lb_csr_t A, lb_schedule_t sched) {
     case LB_SCHED_THREAD_MAPPED: return "thread_mapped_kernel";
     case LB_SCHED_GROUP_MAPPED: return "group_mapped_kernel<32>";
     case LB_SCHED_BLOCK_MAPPED: return "group_mapped_kernel<256>";
+    case LB_SCHED_NONZERO_SPLIT: return "partition_nz_kernel + merge_stream_kernel<8,4,2,u32>";
     case LB_SCHED_MERGE_PATH: {
       if (!A || l_index(A->L) < 0) return "";
       const PipeVariant& v = kVariants[pipe_variant_for(A->L)];
@@ -717,6 +777,14 @@ lb_status_t lb_partition(lb_csr_t A, int32_t items_per_tile, int32_t* d_coords, 
   int64_t L = items_per_tile == 0 ? A->L : items_per_tile;
   if (L <= 0) return fail(LB_ERR_INVALID_ARG, "items_per_tile must be >= 1");
   return launch_partition(A, L, reinterpret_cast<int2*>(d_coords), S(stream));
+}
+
+lb_status_t lb_partition_nz(lb_csr_t A, int32_t items_per_tile, int32_t* d_coords, void* stream) {
+  g_err.clear();
+  if (!A || !d_coords) return fail(LB_ERR_INVALID_ARG, "null argument");
+  const int64_t L = items_per_tile == 0 ? kNzL : items_per_tile;
+  if (L <= 0) return fail(LB_ERR_INVALID_ARG, "items_per_tile must be >= 1");
+  return launch_partition_nz(A, L, reinterpret_cast<int2*>(d_coords), S(stream));
 }
 
 lb_status_t lb_spmv(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_y, void* stream) {

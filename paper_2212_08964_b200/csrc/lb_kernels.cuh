@@ -121,6 +121,31 @@ __global__ void partition_kernel(int rows, int nnz, const int* __restrict__ off,
   coords[t] = make_int2(lo, (int)(d - lo));
 }
 
+// Nonzero-splitting partition (table; reading R19): tiles of L nonzeros, T = max(1,
+// ceil(nnz/L)); boundary t: j = min(t*L, nnz), i = #{r : off[r+1] <= j} (upper bound of j in
+// off[1..rows]), with (0, 0) and (rows, nnz) at the ends.  Every such (i, j) is a merge-path point,
+// so the merge-path tile processors run these tiles unchanged.
+__global__ void partition_nz_kernel(int rows, int nnz, const int* __restrict__ off, int64_t L, int64_t T,
+                                    int2* __restrict__ coords) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > T) return;
+  const int j = (int)(t * L < nnz ? t * L : nnz);
+  int i;
+  if (t == 0) i = 0;
+  else if (t == T) i = rows;
+  else {
+    int lo = 0, hi = rows;  // first r in [0, rows] with off[r+1] > j (r = rows if none)
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (__ldg(off + mid + 1) <= j) lo = mid + 1;
+      else hi = mid;
+    }
+    i = lo;
+  }
+  coords[t] = make_int2(i, j);
+}
+
 // ----------------------------------------------------------------------------- merge-path tiles
 struct MergeArgs {
   const int* off;
@@ -1060,9 +1085,9 @@ __device__ __forceinline__ void stream_prefetch_offsets(const PipeArgs& a, int4 
 // Row pass of tile c into tail[]: tail[q] = r + 1 when local nonzero q ends row r (r >= 0);
 // rows r > 0 with no nonzero in the tile get y = 0; returns (warp-uniform) whether row 0 has no
 // nonzero in the tile (its value is then the carry entering the tile).
-template <int R, int K>
+template <int R, int K, typename TailT>
 __device__ __forceinline__ bool stream_row_pass(const PipeArgs& a, int4 c, int lane, const int (&lo_)[K],
-                                                const int (&hi_)[K], unsigned short* tail) {
+                                                const int (&hi_)[K], TailT* tail) {
   const int i0 = c.x, nrows = c.z - c.x, jA = c.y & ~7, lo = c.y - jA;
   bool row0_empty = false;
   for (int j = 0; 32 * j < nrows; ++j) {
@@ -1079,7 +1104,7 @@ __device__ __forceinline__ bool stream_row_pass(const PipeArgs& a, int4 c, int l
       }
       const int e = oe - jA;
       const int s = r == 0 ? lo : ob - jA;
-      if (e > s) tail[e - 1] = (unsigned short)(r + 1);
+      if (e > s) tail[e - 1] = (TailT)(r + 1);
       else if (r > 0) __stcs(a.y + i0 + r, 0.f);
       else row0_empty = true;
     }
@@ -1087,11 +1112,31 @@ __device__ __forceinline__ bool stream_row_pass(const PipeArgs& a, int4 c, int l
   return __shfl_sync(kFull, (int)row0_empty, 0) != 0;
 }
 
-template <int W, int R, int MINB, bool XKEEP>
+// 8 row ids of a lane's round from the warp's tail buffer (16- or 32-bit entries)
+__device__ __forceinline__ void tail_read8(const unsigned short* p, unsigned (&rid)[8]) {
+  const uint4 q = *reinterpret_cast<const uint4*>(p);
+  const unsigned w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int e = 0; e < 8; ++e) rid[e] = (e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xFFFFu);
+}
+__device__ __forceinline__ void tail_read8(const unsigned* p, unsigned (&rid)[8]) {
+  const uint4 q0 = *reinterpret_cast<const uint4*>(p), q1 = *reinterpret_cast<const uint4*>(p + 4);
+  rid[0] = q0.x; rid[1] = q0.y; rid[2] = q0.z; rid[3] = q0.w;
+  rid[4] = q1.x; rid[5] = q1.y; rid[6] = q1.z; rid[7] = q1.w;
+}
+__device__ __forceinline__ void tail_clear8(unsigned short* p) { *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u); }
+__device__ __forceinline__ void tail_clear8(unsigned* p) {
+  *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
+  *reinterpret_cast<uint4*>(p + 4) = make_uint4(0u, 0u, 0u, 0u);
+}
+
+// TailT: unsigned short for merge-path tiles (<= L rows), unsigned for nonzero-split tiles (any
+// number of rows per tile).
+template <int W, int R, int MINB, bool XKEEP, typename TailT = unsigned short>
 __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) {
   using Cfg = StreamCfg<R>;
   constexpr int K = Cfg::K;
-  __shared__ __align__(16) unsigned short s_tail[W][Cfg::kCap];
+  __shared__ __align__(16) TailT s_tail[W][Cfg::kCap];
   __shared__ int s_last;
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1100,8 +1145,9 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
   const int t_end = min(a.num_tiles, t_begin + a.tiles_per_cta);
   const uint64_t spol = policy_evict_first();
   const uint64_t xpol = XKEEP ? policy_evict_last() : 0ull;
-  unsigned short* tail = s_tail[warp];
-  for (int w = lane; w < Cfg::kCap / 8; w += 32) reinterpret_cast<uint4*>(tail)[w] = make_uint4(0u, 0u, 0u, 0u);
+  TailT* tail = s_tail[warp];
+  for (int w = lane; w < Cfg::kCap * (int)sizeof(TailT) / 16; w += 32)
+    reinterpret_cast<uint4*>(tail)[w] = make_uint4(0u, 0u, 0u, 0u);
   asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: coords are read below
   __syncwarp();
 
@@ -1115,7 +1161,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
     int4 cT2 = t_begin + 2 < t_end ? tile_coords(a, t_begin + 2) : cT1;
     int olo[K], ohi[K];
     stream_prefetch_offsets<R, K>(a, cT, lane, olo, ohi);
-    bool r0e = stream_row_pass<R, K>(a, cT, lane, olo, ohi, tail);
+    bool r0e = stream_row_pass<R, K, TailT>(a, cT, lane, olo, ohi, tail);
     if (t_begin + 1 < t_end) stream_prefetch_offsets<R, K>(a, cT1, lane, olo, ohi);
     __syncwarp();
     // pipeline registers: step s (gathered), s+1 (gathered next), s+2 (loading)
@@ -1144,14 +1190,16 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
         rc = 0.f;
       }
       // (c) reduce this round
-      const uint4 tq = *reinterpret_cast<const uint4*>(&tail[256 * k + 8 * lane]);
-      const unsigned tr[4] = {tq.x, tq.y, tq.z, tq.w};
+      unsigned rids[8];
+      tail_read8(&tail[256 * k + 8 * lane], rids);
+      unsigned any = 0u;
       float run = 0.f, first_val = 0.f;
       int first_r = -1;
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         run = fmaf(d0.val[e], x0[e], run);
-        const unsigned rid = (e & 1) ? (tr[e >> 1] >> 16) : (tr[e >> 1] & 0xFFFFu);
+        const unsigned rid = rids[e];
+        any |= rid;
         if (rid) {
           const int r = (int)rid - 1;
           if (first_r < 0) { first_r = r; first_val = run; }
@@ -1170,8 +1218,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
         const float carry_in = lane == 0 ? rc : (lf ? lval : rc + lval);
         __stcs(a.y + i0 + first_r, carry_in + first_val);
       }
-      if (tr[0] | tr[1] | tr[2] | tr[3])
-        *reinterpret_cast<uint4*>(&tail[256 * k + 8 * lane]) = make_uint4(0u, 0u, 0u, 0u);
+      if (any) tail_clear8(&tail[256 * k + 8 * lane]);
       rc = agg_f ? agg_v : rc + agg_v;
       // (d) rotate the pipeline
 #pragma unroll
@@ -1181,7 +1228,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
         ++t;
         __syncwarp();
         if (t < t_end) {
-          r0e = stream_row_pass<R, K>(a, cT1, lane, olo, ohi, tail);
+          r0e = stream_row_pass<R, K, TailT>(a, cT1, lane, olo, ohi, tail);
           if (t + 1 < t_end) stream_prefetch_offsets<R, K>(a, cT2, lane, olo, ohi);
           cT = cT1;
           cT1 = cT2;

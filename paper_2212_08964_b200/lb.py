@@ -19,7 +19,8 @@ LIB_PATH = os.environ.get("LB_LIB_PATH") or os.path.join(_PKG, "liblb.so")
 HEADER = os.path.join(_ROOT, "include", "lb.h")
 
 LB_OK, LB_ERR_INVALID_ARG, LB_ERR_INVALID_CSR, LB_ERR_UNSUPPORTED, LB_ERR_OOM, LB_ERR_CUDA, LB_ERR_NCCL = range(7)
-SCHEDULES = {"thread_mapped": 0, "group_mapped": 1, "merge_path": 2, "block_mapped": 3, "auto": 4}
+SCHEDULES = {"thread_mapped": 0, "group_mapped": 1, "merge_path": 2, "block_mapped": 3, "auto": 4,
+             "nonzero_split": 5}
 SCHEDULE_NAMES = {v: k for k, v in SCHEDULES.items()}
 LB_SPMV_REPARTITION = 1
 DEFAULT_ITEMS_PER_TILE = 1016
@@ -63,6 +64,7 @@ def lib() -> ctypes.CDLL:
         "lb_csr_set_items_per_tile": ([p, i32], st),
         "lb_partition_size": ([p, i32, ctypes.POINTER(i64)], st),
         "lb_partition": ([p, i32, p, p], st),
+        "lb_partition_nz": ([p, i32, p, p], st),
         "lb_spmv": ([p, ctypes.c_int, p, p, p], st),
         "lb_spmv_ex": ([p, ctypes.c_int, p, p, u32, p], st),
         "lb_spmm": ([p, i64, p, i64, p, i64, p], st),
@@ -195,6 +197,14 @@ class CsrMatrix:
             out = torch.empty((T + 1, 2), dtype=torch.int32, device=self.device)
         _dev_tensor(out, torch.int32, "out", 2 * (T + 1))
         _check(lib().lb_partition(self.handle, int(items_per_tile), out.data_ptr(), _stream(stream)))
+        return out
+
+    def partition_nz(self, items_per_tile: int = 1016, stream=None) -> torch.Tensor:
+        """Nonzero-splitting tile coordinates, int32 [T+1, 2] of (row, nz) (lb_partition_nz)."""
+        L = int(items_per_tile) or 1016
+        T = max(1, (self.nnz + L - 1) // L)
+        out = torch.empty((T + 1, 2), dtype=torch.int32, device=self.device)
+        _check(lib().lb_partition_nz(self.handle, L, out.data_ptr(), _stream(stream)))
         return out
 
     def spmv(self, x: torch.Tensor, y: torch.Tensor | None = None, schedule="merge_path",

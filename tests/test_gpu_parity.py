@@ -20,7 +20,7 @@ import paper_2212_08964_b200 as lb
 
 pytestmark = pytest.mark.gpu
 
-SCHEDS = ["merge_path", "thread_mapped", "group_mapped", "block_mapped", "auto"]
+SCHEDS = ["merge_path", "thread_mapped", "group_mapped", "block_mapped", "auto", "nonzero_split"]
 TOL = 1e-5
 
 
@@ -476,3 +476,28 @@ def test_spmm_full_size(cfg):
         check_y(Yh[:, j], y_ref, s_ref, True, f"{cfg} col {j}")
     del M, A, X, Y
     torch.cuda.empty_cache()
+
+
+
+# ---------------------------------------------------------------- nonzero-split partition (NEXT-3)
+
+@pytest.mark.parametrize("L", [1, 3, 64, 1016])
+@pytest.mark.parametrize("name", ["rmat12", "stencil100", "skewed", "c1"])
+def test_partition_nz_bit_exact(name, L):
+    A = SMALL[name]("int")
+    M = lb.CsrMatrix.from_csr(A)
+    assert np.array_equal(M.partition_nz(L).cpu().numpy(), oracle.partition_nz(A.row_offsets, L))
+
+
+def test_nonzero_split_many_empty_rows():
+    """Tiles spanning >65535 empty rows (32-bit row ids) and long empty runs between nonzeros."""
+    rows = 200_000
+    lens = np.zeros(rows, np.int64)
+    lens[[5, 70_000, 70_001, 150_000, rows - 1]] = [3, 2000, 1, 5, 7]
+    off = np.zeros(rows + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    A = _csr(off.tolist(), 4, col=[0] * int(off[-1]), val=[1.0] * int(off[-1]))
+    x = torch.ones(4)
+    y_ref, s_ref = ref(A, x)
+    for sched in ("nonzero_split", "merge_path"):
+        check_y(run(A, x, sched), y_ref, s_ref, True, sched)

@@ -342,3 +342,28 @@ def test_spmm_identity_closed_form():
     X = lbgen.make_x(n * 5, "float", 3).numpy().reshape(n, 5)
     Y, _ = oracle.spmm(off, np.arange(n, dtype=np.int32), np.ones(n, np.float32), X)
     assert np.array_equal(Y, X.astype(np.float64))
+
+
+# ---------------------------------------------------------------- nonzero-split (NEXT-3) pins
+
+def test_partition_nz_worked_example_and_merge_path_points():
+    """Hand-derived: off = [0,1,3,3,6], L = 2 -> j = 0,2,4,6; rows ending at or before j:
+    j=2 -> rows 0 (end 1); j=4 -> rows 0,1,2 (ends 1,3,3); last = (4, 6)."""
+    c = oracle.partition_nz(np.array([0, 1, 3, 3, 6], np.int32), 2)
+    assert c.tolist() == [[0, 0], [1, 2], [3, 4], [4, 6]]
+    # every nonzero-split coordinate is a point on the merge path: off[i] <= j <= off[i+1] for i < rows
+    rng = np.random.default_rng(4)
+    for trial in range(200):
+        A = random_csr(rng, int(rng.integers(0, 60)), 20, int(rng.integers(0, 9)), float(rng.random()), "int")
+        off = A.row_offsets.numpy().astype(np.int64)
+        for L in (1, 3, 16):
+            c = oracle.partition_nz(A.row_offsets, L).astype(np.int64)
+            i, j = c[:, 0], c[:, 1]
+            assert tuple(c[0]) == (0, 0) and tuple(c[-1]) == (A.rows, A.nnz)
+            assert np.all(np.diff(i) >= 0) and np.all(np.diff(j) >= 0)
+            assert np.all(np.diff(j)[:-1] == L) if c.shape[0] > 2 else True
+            inner = i < A.rows
+            assert np.all(off[i[inner]] <= j[inner]) and np.all(j[inner] <= off[i[inner] + 1])
+            # i_t (0 < t < T) is the closed-form count #{r : off[r+1] <= j_t}
+            for t in range(1, c.shape[0] - 1):
+                assert i[t] == np.count_nonzero(off[1:] <= j[t])
