@@ -262,6 +262,16 @@ def run_single(args, cfg):
                      "peak_source": peak_src,
                      "kernel_ms_from": "mean of 20 lb_spmv_phase_times calls (CUDA events on the launch stream)"},
     }
+    # the stream+gather ceiling of this matrix on this GPU (no row structure), measured live
+    try:
+        probe_ms = M.probe_stream_gather(x, reps=20)
+        rec["roofline_gather"] = {
+            "bound": "l1tex gather (1 L1->L2 request per clock per SM for random 4-byte x[col])",
+            "achieved": round(nnz / (main_ms * 1e-3) / 1e9, 2), "peak": round(nnz / (probe_ms * 1e-3) / 1e9, 2),
+            "unit": "GNZ/s", "frac": round(probe_ms / main_ms, 4),
+            "peak_source": "lb_probe_stream_gather: same col/val/x, 256-bit stream loads + gathers, no rows"}
+    except Exception as e:  # pragma: no cover
+        rec["roofline_gather"] = {"error": str(e)}
     if args.no_extras:
         print(json.dumps(rec))
         return

@@ -200,6 +200,15 @@ lb_status_t lb_spmv_phase_times(lb_csr_t A, lb_schedule_t sched, const float* d_
                                 float* ms_out);
 
 /*
+ * lb_probe_stream_gather -- diagnostics: time (CUDA events, synchronises `stream`) a kernel that
+ * streams A's col_idx/values with the tile processor's 256-bit loads and gathers x[col] with no
+ * row structure, `reps` times; ms_out = mean milliseconds per pass.  nnz / ms_out is the
+ * stream+gather ceiling for this matrix on this GPU (the bound of the merge-path tile processor
+ * on random-column matrices).  Needs 32-byte aligned col_idx/values.
+ */
+lb_status_t lb_probe_stream_gather(lb_csr_t A, const float* d_x, int32_t reps, void* stream, float* ms_out);
+
+/*
  * lb_shard_bounds -- host-only: row-shard bounds for `nranks` GPUs with equal nonzeros
  * (reading R9; the paper defers multi-GPU to future work):
  *   b_0 = 0, b_G = rows, b_g = min{ r : off[r] >= ceil(g * nnz / G) }   (0 < g < G).

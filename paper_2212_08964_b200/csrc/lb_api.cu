@@ -779,6 +779,39 @@ lb_status_t lb_partition(lb_csr_t A, int32_t items_per_tile, int32_t* d_coords, 
   return launch_partition(A, L, reinterpret_cast<int2*>(d_coords), S(stream));
 }
 
+lb_status_t lb_probe_stream_gather(lb_csr_t A, const float* d_x, int32_t reps, void* stream, float* ms_out) {
+  g_err.clear();
+  if (!A || !ms_out || reps < 1 || (!d_x && A->nnz > 0)) return fail(LB_ERR_INVALID_ARG, "bad probe arguments");
+  if (!A->vec32) return fail(LB_ERR_UNSUPPORTED, "probe needs 32-byte aligned col_idx/values");
+  stream_t s = S(stream);
+  static int blocks_cache[64] = {0};
+  int& blocks = blocks_cache[A->device];
+  if (blocks == 0) {
+    LB_CUDA(cudaFuncSetAttribute(lbk::probe_stream_gather_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
+    LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, lbk::probe_stream_gather_kernel, kNT, 0));
+    blocks = std::max(1, blocks);
+  }
+  const int grid = A->dev->sm_count * blocks;
+  cudaEvent_t e0, e1;
+  LB_CUDA(cudaEventCreate(&e0));
+  LB_CUDA(cudaEventCreate(&e1));
+  lbk::probe_stream_gather_kernel<<<grid, kNT, 0, s>>>((int)A->nnz, A->col, A->val, d_x, 0, nullptr);  // warm-up
+  LB_LAUNCHED();
+  LB_CUDA(cudaEventRecord(e0, s));
+  for (int r = 0; r < reps; ++r) {
+    lbk::probe_stream_gather_kernel<<<grid, kNT, 0, s>>>((int)A->nnz, A->col, A->val, d_x, 0, nullptr);
+    LB_LAUNCHED();
+  }
+  LB_CUDA(cudaEventRecord(e1, s));
+  LB_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  LB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  *ms_out = ms / reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return LB_OK;
+}
+
 lb_status_t lb_partition_nz(lb_csr_t A, int32_t items_per_tile, int32_t* d_coords, void* stream) {
   g_err.clear();
   if (!A || !d_coords) return fail(LB_ERR_INVALID_ARG, "null argument");

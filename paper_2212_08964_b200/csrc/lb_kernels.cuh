@@ -1267,6 +1267,32 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
   }
 }
 
+// ----------------------------------------------------------------------------- ceiling probe
+// Diagnostic: stream col/val with the tile kernels' 256-bit loads and gather x[col] with no row
+// structure (no scans, no y) -- the stream+gather ceiling of this matrix on this GPU, against which
+// bench.py reports the tile processor.  `flag` is 0 at run time (keeps the sum live).
+__global__ void __launch_bounds__(256) probe_stream_gather_kernel(int nnz, const int* __restrict__ col,
+                                                                  const float* __restrict__ val,
+                                                                  const float* __restrict__ x, int flag,
+                                                                  float* sink) {
+  const uint64_t pol = policy_evict_first();
+  float s = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 8;
+  int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  for (; i + 8 <= nnz; i += stride) {
+    int c[8];
+    float v[8], xv[8];
+    ld_stream_v8(col + i, c, pol);
+    ld_stream_v8(val + i, v, pol);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) xv[e] = ld_x(x + c[e]);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s = fmaf(v[e], xv[e], s);
+  }
+  for (; i < nnz; ++i) s = fmaf(val[i], x[col[i]], s);
+  if (flag) sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 // ----------------------------------------------------------------------------- SpMM (NEXT-2)
 // Y = A X for a panel of P (1 or 4) columns of a row-major X (Listing 4: "a simple loop
 // wrapped around SpMV"), on the same merge-path tiles as SpMV (L = 1016, lb_partition's output is

@@ -71,6 +71,7 @@ def lib() -> ctypes.CDLL:
         "lb_spmv_host_workspace_size": ([i64, i64, i64], sz),
         "lb_spmv_host": ([i64, i64, i64, p, p, p, p, p, ctypes.c_int, p, sz, p], st),
         "lb_spmv_phase_times": ([p, ctypes.c_int, p, p, p, ctypes.POINTER(ctypes.c_float)], st),
+        "lb_probe_stream_gather": ([p, p, i32, p, ctypes.POINTER(ctypes.c_float)], st),
         "lb_shard_bounds": ([p, i64, i32, p], st),
         "lb_comm_unique_id": ([p], st),
         "lb_comm_init": ([p, i32, i32, i32, ctypes.POINTER(p)], st),
@@ -239,6 +240,12 @@ class CsrMatrix:
         _check(lib().lb_spmm(self.handle, n, X.data_ptr() if X.numel() else None, max(X.stride(0), n),
                              Y.data_ptr() if Y.numel() else None, max(Y.stride(0), n), _stream(stream)))
         return Y
+
+    def probe_stream_gather(self, x: torch.Tensor, reps: int = 20, stream=None) -> float:
+        """Milliseconds of one stream+gather pass over this matrix (lb_probe_stream_gather)."""
+        ms = ctypes.c_float()
+        _check(lib().lb_probe_stream_gather(self.handle, x.data_ptr(), int(reps), _stream(stream), ctypes.byref(ms)))
+        return float(ms.value)
 
     def kernel_name(self, schedule="merge_path") -> str:
         """Main kernel lb_spmv launches for `schedule` (lb_kernel_name)."""
