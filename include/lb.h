@@ -171,6 +171,39 @@ lb_status_t lb_select_schedule(lb_csr_t A, void* stream, lb_schedule_t* out);
  */
 lb_status_t lb_spmm(lb_csr_t A, int64_t n, const float* d_X, int64_t ldx, float* d_Y, int64_t ldy, void* stream);
 
+/*
+ * lb_csr_plan_hot_x -- hot-column plan for MERGE_PATH (B200 extension; not in the paper -- DESIGN.md
+ * section 6b).  Background: a merge-path tile reads col/val as a stream but x[col] as random 4-byte
+ * gathers (Listing 3 P:980 `x[column_indices[nz]]`), and on B200 gathers that miss L1 are served at
+ * about one L1TEX line per clock per SM, while shared memory serves random reads several times
+ * faster.  The plan:
+ *   deg(c)   = number of stored entries in column c; candidates = columns with deg(c) >= 2;
+ *   fewer than `slots` candidates: all are hot, slots numbered in ascending column order;
+ *   otherwise: the hot set is the first `slots` candidates ordered by (deg descending, column
+ *              ascending); with tau = the smallest degree in it, slots go first to the hot
+ *              columns with deg > tau, then to those with deg == tau, each in ascending column order;
+ *   a private copy of col_idx in which every entry of a hot column c holds ~slot(c) (< 0).
+ * With a plan, every lb_spmv(MERGE_PATH) call (L = 504 or 1016) gathers x of the hot columns once,
+ * each CTA stages them in shared memory, and the tile kernel reads hot x values from there.  The
+ * products and the summation order are unchanged: y is bitwise identical to the call without a
+ * plan.  Other schedules ignore the plan.
+ *  slots          0 = default (32768: 128 KB of shared memory per SM); 1 .. 45056; < 0 drops the plan.
+ *  hot_cols_out   (optional) number of planned hot columns (0: no plan was kept).
+ *  hot_nnz_out    (optional) number of stored entries in hot columns.
+ * Cost: device memory 4*nnz + 8*hot + 4*cols (temporary); a degree histogram, 1-4 selection passes
+ * and a remap of col_idx; synchronises `stream`.  The caller's arrays are not modified.  Errors:
+ * LB_ERR_UNSUPPORTED if col_idx/values are not 32-byte aligned; LB_ERR_OOM.  Re-plan (or drop the
+ * plan) after modifying col_idx.
+ */
+lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, void* stream, int32_t* hot_cols_out, int64_t* hot_nnz_out);
+
+/* lb_csr_hot_plan -- inspect the plan (tests): *hot_n = number of hot columns (0: no plan),
+ * *hot_nnz = their stored entries; when a plan exists and the pointers are non-NULL, copies (stream-
+ * ordered, device to device) the slot -> column table into d_hot_cols_out int32[hot_n] and the
+ * remapped column stream into d_hot_col_idx_out int32[nnz] (caller-owned device buffers). */
+lb_status_t lb_csr_hot_plan(lb_csr_t A, int32_t* hot_n, int64_t* hot_nnz, int32_t* d_hot_cols_out,
+                            int32_t* d_hot_col_idx_out, void* stream);
+
 /* Flags for lb_spmv_ex. */
 #define LB_SPMV_REPARTITION 1u /* MERGE_PATH: recompute the partition inside this call */
 

@@ -254,6 +254,14 @@ struct lb_csr_s {
   int* flags = nullptr;       // [4] validation flags
   unsigned* ticket = nullptr; // [1] last-CTA ticket of the pipelined kernel (kept at 0 between launches)
   int max_row = -1;           // longest row (LB_SCHED_AUTO), -1 until computed
+  // hot-column plan (lb_csr_plan_hot_x; one allocation at plan_mem)
+  void* plan_mem = nullptr;
+  int32_t* hcol = nullptr;     // [nnz] col_idx with hot entries replaced by ~slot
+  int32_t* hot_cols = nullptr; // [hot_n] slot -> column
+  float* x_hot = nullptr;      // [hot_n4 * 4] x of the hot columns, gathered every call
+  int hot_n = 0;               // planned hot columns (0: no plan)
+  int hot_n4 = 0;              // ceil(hot_n / 4)
+  int64_t hot_nnz = 0;         // stored entries in hot columns
 };
 
 namespace {
@@ -506,6 +514,193 @@ lb_status_t launch_nz_tiles(lb_csr_s* A, const float* x, float* y, stream_t s) {
   return LB_OK;
 }
 
+// ----------------------------------------------------------------------------- hot-column plan
+// Tile kernel with the plan: warp-streamed, one CTA of W warps per SM, x of the hot columns staged
+// in dynamic shared memory.  W and the slot budget were chosen by measurement;
+// LB_HOT_W overrides W (8, 16, 20) for sweeps.
+constexpr int kHotSlotsDefault = 32768;  // 128 KB of shared memory per SM
+constexpr int kHotSlotsMax = 45056;      // 176 KB
+constexpr int kHotDynMax = kHotSlotsMax * 4;
+
+template <int W, int R>
+lb_status_t hot_launch_wr(lb_csr_s* A, const float* x, float* y, stream_t s) {
+  auto k = lbk::merge_stream_kernel<W, R, 1, false, unsigned short, true>;
+  static int conf_dyn[64] = {0};  // dynamic smem size the carve-out was set for, per device
+  const int dyn = A->hot_n4 * 16;
+  if (conf_dyn[A->device] != dyn) {
+    cudaFuncAttributes fa;
+    LB_CUDA(cudaFuncGetAttributes(&fa, k));
+    LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kHotDynMax));
+    const double need = (double)fa.sharedSizeBytes + dyn + 1024.0;
+    const int pct = std::min(100, std::max(1, (int)(100.0 * need / (228.0 * 1024.0)) + 1));
+    LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    int blocks = 0;
+    LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, W * 32, dyn));
+    if (blocks < 1) return fail(LB_ERR_UNSUPPORTED, "hot tile kernel does not fit with %d bytes of x_hot", dyn);
+    conf_dyn[A->device] = dyn;
+  }
+  constexpr int L = 256 * R - 8;
+  const int T = (int)num_tiles(A->rows, A->nnz, L);
+  const int warps_max = std::min(A->dev->sm_count * W, kMaxCtas);
+  const int tpw = (T + warps_max - 1) / warps_max;
+  const int warps = (T + tpw - 1) / tpw;
+  const int grid = (warps + W - 1) / W;
+  lbk::PipeArgs a;
+  a.off = A->off; a.col = A->hcol; a.val = A->val; a.x = x; a.y = y;
+  a.coords = A->coords; a.rows = (int)A->rows; a.nnz = (int)A->nnz;
+  a.num_tiles = T; a.tiles_per_cta = tpw;
+  a.carry_row = A->carry_row; a.carry_val = A->carry_val; a.ticket = A->ticket;
+  a.x_hot = A->x_hot; a.hot_n4 = A->hot_n4;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(W * 32);
+  cfg.dynamicSmemBytes = (size_t)dyn;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL after partition_xhot_kernel
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  LB_CUDA(cudaLaunchKernelEx(&cfg, k, a));
+  LB_LAUNCHED();
+  return LB_OK;
+}
+
+int hot_warps() {
+  const char* env = getenv("LB_HOT_W");
+  const int w = env ? atoi(env) : 16;
+  return (w == 8 || w == 16 || w == 20) ? w : 16;
+}
+
+bool hot_usable(const lb_csr_s* A) { return A->hot_n > 0 && A->vec32 && (A->L == 1016 || A->L == 504); }
+
+lb_status_t hot_launch(lb_csr_s* A, const float* x, float* y, stream_t s) {
+  const int w = hot_warps();
+  if (A->L == 1016) {
+    if (w == 8) return hot_launch_wr<8, 4>(A, x, y, s);
+    if (w == 20) return hot_launch_wr<20, 4>(A, x, y, s);
+    return hot_launch_wr<16, 4>(A, x, y, s);
+  }
+  if (w == 8) return hot_launch_wr<8, 2>(A, x, y, s);
+  if (w == 20) return hot_launch_wr<20, 2>(A, x, y, s);
+  return hot_launch_wr<16, 2>(A, x, y, s);
+}
+
+// partition (T >= 0) and/or the x_hot gather in one launch
+lb_status_t launch_partition_xhot(const lb_csr_s* A, int64_t L, bool partition, const float* x, stream_t s) {
+  const int64_t T = partition ? num_tiles(A->rows, A->nnz, L) : -1;
+  const int64_t n = T + 1 + A->hot_n;
+  const int grid = (int)std::max<int64_t>(1, (n + kNT - 1) / kNT);
+  lbk::partition_xhot_kernel<<<grid, kNT, 0, s>>>((int)A->rows, (int)A->nnz, A->off, L, T, A->coords, A->hot_cols,
+                                                   A->hot_n, x, A->x_hot);
+  LB_LAUNCHED();
+  return LB_OK;
+}
+
+void drop_plan(lb_csr_s* A) {
+  if (A->plan_mem) cudaFree(A->plan_mem);
+  A->plan_mem = nullptr;
+  A->hcol = A->hot_cols = nullptr;
+  A->x_hot = nullptr;
+  A->hot_n = A->hot_n4 = 0;
+  A->hot_nnz = 0;
+}
+
+// Builds the plan (see lb.h lb_csr_plan_hot_x).  Synchronises `s` a few times (setup call).
+lb_status_t build_plan(lb_csr_s* A, int slots, stream_t s) {
+  drop_plan(A);
+  const int cols = (int)A->cols;
+  const int64_t nnz = A->nnz;
+  const int nblk = (int)((A->cols + lbk::kHotChunk - 1) / lbk::kHotChunk);
+  // temporaries: deg/smap [cols], bins [kDegBins], block offsets [nblk], totals + hot_nnz
+  const size_t tmp_bytes = align256((size_t)cols * 4) + align256(lbk::kDegBins * 4) + align256((size_t)nblk * 8) +
+                           align256(16) + align256(8);
+  char* tmp = nullptr;
+  if (cudaMalloc(&tmp, tmp_bytes) != cudaSuccess) { cudaGetLastError(); return fail(LB_ERR_OOM, "plan temporaries"); }
+  struct Free { char* p; ~Free() { cudaFree(p); } } free_tmp{tmp};
+  int* deg = reinterpret_cast<int*>(tmp);
+  int* bins = reinterpret_cast<int*>(tmp + align256((size_t)cols * 4));
+  int2* blk = reinterpret_cast<int2*>(reinterpret_cast<char*>(bins) + align256(lbk::kDegBins * 4));
+  int* totals = reinterpret_cast<int*>(reinterpret_cast<char*>(blk) + align256((size_t)nblk * 8));
+  unsigned long long* d_hot_nnz = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(totals) + align256(16));
+
+  const int sms = A->dev->sm_count;
+  LB_CUDA(cudaMemsetAsync(deg, 0, (size_t)cols * 4, s));
+  lbk::col_degree_kernel<<<sms * 8, kNT, 0, s>>>(nnz, A->col, deg);
+  LB_LAUNCHED();
+
+  // threshold: the degree tau of the slots-th hottest column (columns with >= 2 entries only), by
+  // successive equal-width histograms over the candidate degree range [lo, hi)
+  int64_t lo = 2, hi = nnz + 1, above = 0;  // above = #columns with deg >= hi
+  int t_hi = 2, t_tie = -1, tie_budget = 0;
+  std::vector<int> hb(lbk::kDegBins);
+  const int hgrid = std::max(1, std::min(sms * 4, (cols + kNT - 1) / kNT));
+  while (true) {
+    if (hi <= lo) { t_hi = (int)lo; break; }
+    const int64_t w = (hi - lo + lbk::kDegBins - 1) / lbk::kDegBins;
+    LB_CUDA(cudaMemsetAsync(bins, 0, lbk::kDegBins * 4, s));
+    lbk::degree_hist_kernel<<<hgrid, kNT, 0, s>>>(cols, deg, lo, hi, w, bins);
+    LB_LAUNCHED();
+    LB_CUDA(cudaMemcpyAsync(hb.data(), bins, lbk::kDegBins * 4, cudaMemcpyDeviceToHost, s));
+    LB_CUDA(cudaStreamSynchronize(s));
+    int64_t cum = above;
+    int found = -1;
+    for (int b = lbk::kDegBins - 1; b >= 0; --b) {
+      if (lo + (int64_t)b * w >= hi) continue;
+      if (cum + hb[b] >= slots) { found = b; break; }
+      cum += hb[b];
+    }
+    if (found < 0) { t_hi = (int)lo; break; }  // fewer candidates than slots: all of them
+    const int64_t nlo = lo + (int64_t)found * w, nhi = std::min(hi, nlo + w);
+    above = cum;
+    if (w == 1) {  // tau = nlo: columns above it all fit; ties fill the remaining slots in column order
+      t_hi = (int)(nlo + 1);
+      t_tie = (int)nlo;
+      tie_budget = (int)(slots - above);
+      break;
+    }
+    lo = nlo;
+    hi = nhi;
+  }
+
+  lbk::hot_count_kernel<<<nblk, 256, 0, s>>>(cols, deg, t_hi, t_tie, blk);
+  LB_LAUNCHED();
+  lbk::hot_scan_kernel<<<1, 1024, 0, s>>>(nblk, blk, totals);
+  LB_LAUNCHED();
+  int tot[2];
+  LB_CUDA(cudaMemcpyAsync(tot, totals, sizeof tot, cudaMemcpyDeviceToHost, s));
+  LB_CUDA(cudaStreamSynchronize(s));
+  const int n_above = tot[0];
+  const int hot_n = n_above + std::min(tie_budget, tot[1]);
+  if (hot_n == 0) return LB_OK;  // nothing worth caching: no plan
+
+  const int hot_n4 = (hot_n + 3) / 4;
+  const size_t plan_bytes = align256((size_t)nnz * 4) + align256((size_t)hot_n * 4) + align256((size_t)hot_n4 * 16);
+  void* pm = nullptr;
+  if (cudaMalloc(&pm, plan_bytes) != cudaSuccess) { cudaGetLastError(); return fail(LB_ERR_OOM, "plan (%zu bytes)", plan_bytes); }
+  char* q = static_cast<char*>(pm);
+  int32_t* hcol = reinterpret_cast<int32_t*>(q);
+  int32_t* hot_cols = reinterpret_cast<int32_t*>(q + align256((size_t)nnz * 4));
+  float* x_hot = reinterpret_cast<float*>(q + align256((size_t)nnz * 4) + align256((size_t)hot_n * 4));
+  LB_CUDA(cudaMemsetAsync(x_hot, 0, (size_t)hot_n4 * 16, s));
+  LB_CUDA(cudaMemsetAsync(d_hot_nnz, 0, 8, s));
+  lbk::hot_assign_kernel<<<nblk, 256, 0, s>>>(cols, deg, t_hi, t_tie, n_above, tie_budget, blk, hot_cols, d_hot_nnz);
+  LB_LAUNCHED();
+  lbk::hot_remap_kernel<<<sms * 8, kNT, 0, s>>>(nnz, A->col, deg, hcol);
+  LB_LAUNCHED();
+  unsigned long long hn = 0;
+  LB_CUDA(cudaMemcpyAsync(&hn, d_hot_nnz, 8, cudaMemcpyDeviceToHost, s));
+  LB_CUDA(cudaStreamSynchronize(s));
+  A->plan_mem = pm;
+  A->hcol = hcol;
+  A->hot_cols = hot_cols;
+  A->x_hot = x_hot;
+  A->hot_n = hot_n;
+  A->hot_n4 = hot_n4;
+  A->hot_nnz = (int64_t)hn;
+  return LB_OK;
+}
+
 template <int L>
 lb_status_t launch_merge(lb_csr_s* A, const float* x, float* y, stream_t s, PhaseEvents* pe) {
   const int li = l_index(L);
@@ -587,7 +782,16 @@ lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y
     }
     case LB_SCHED_MERGE_PATH: {
       lb_status_t st;
-      if (!A->coords_valid || A->coords_kind != 0 || A->coords_L != A->L || (flags & LB_SPMV_REPARTITION)) {
+      const bool repart = !A->coords_valid || A->coords_kind != 0 || A->coords_L != A->L || (flags & LB_SPMV_REPARTITION);
+      if (hot_usable(A)) {  // hot-column plan: partition + x_hot gather in one launch, then the hot tile kernel
+        if ((st = launch_partition_xhot(A, A->L, repart, x, s)) != LB_OK) return st;
+        if (repart) { A->coords_valid = true; A->coords_L = A->L; A->coords_kind = 0; }
+        if (pe) LB_CUDA(cudaEventRecord(pe->ev[1], s));
+        if ((st = hot_launch(A, x, y, s)) != LB_OK) return st;
+        if (pe) { LB_CUDA(cudaEventRecord(pe->ev[2], s)); LB_CUDA(cudaEventRecord(pe->ev[3], s)); }
+        return LB_OK;
+      }
+      if (repart) {
         if ((st = launch_partition(A, A->L, A->coords, s)) != LB_OK) return st;
         A->coords_valid = true;
         A->coords_L = A->L;
@@ -703,6 +907,10 @@ const char* lb_kernel_name(lb_csr_t A, lb_schedule_t sched) {
     case LB_SCHED_NONZERO_SPLIT: return "partition_nz_kernel + merge_stream_kernel<8,4,2,u32>";
     case LB_SCHED_MERGE_PATH: {
       if (!A || l_index(A->L) < 0) return "";
+      if (hot_usable(A)) {
+        snprintf(buf, sizeof buf, "merge_stream_kernel<%d,%d,1,hot>", hot_warps(), (A->L + 8) / 256);
+        return buf;
+      }
       const PipeVariant& v = kVariants[pipe_variant_for(A->L)];
       const bool ok = v.kind == 0 ? A->vec : v.kind == 1 ? A->pipe : A->vec32;
       if (!ok) { snprintf(buf, sizeof buf, "merge_tile_kernel<256,%d> + fixup_kernel", A->L); return buf; }
@@ -750,6 +958,7 @@ lb_status_t lb_csr_create(int64_t rows, int64_t cols, int64_t nnz, const int32_t
 lb_status_t lb_csr_destroy(lb_csr_t A) {
   if (!A) return LB_OK;
   if (A->owns_scratch && A->coords) cudaFree(A->coords);
+  if (A->plan_mem) cudaFree(A->plan_mem);
   delete A;
   return LB_OK;
 }
@@ -809,6 +1018,42 @@ lb_status_t lb_probe_stream_gather(lb_csr_t A, const float* d_x, int32_t reps, v
   *ms_out = ms / reps;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
+  return LB_OK;
+}
+
+lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, void* stream, int32_t* hot_cols_out, int64_t* hot_nnz_out) {
+  g_err.clear();
+  if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
+  if (slots < 0) {
+    drop_plan(A);
+  } else {
+    if (slots == 0) slots = kHotSlotsDefault;
+    if (slots > kHotSlotsMax) return fail(LB_ERR_INVALID_ARG, "slots %d > %d", slots, kHotSlotsMax);
+    if (!A->vec32) return fail(LB_ERR_UNSUPPORTED, "hot-column plan needs 32-byte aligned col_idx/values");
+    if (A->nnz == 0 || A->cols == 0) {
+      drop_plan(A);
+    } else {
+      lb_status_t st = build_plan(A, slots, S(stream));
+      if (st != LB_OK) { drop_plan(A); return st; }
+    }
+  }
+  if (hot_cols_out) *hot_cols_out = A->hot_n;
+  if (hot_nnz_out) *hot_nnz_out = A->hot_nnz;
+  return LB_OK;
+}
+
+lb_status_t lb_csr_hot_plan(lb_csr_t A, int32_t* hot_n, int64_t* hot_nnz, int32_t* d_hot_cols_out,
+                            int32_t* d_hot_col_idx_out, void* stream) {
+  g_err.clear();
+  if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
+  if (hot_n) *hot_n = A->hot_n;
+  if (hot_nnz) *hot_nnz = A->hot_nnz;
+  if (A->hot_n > 0) {
+    if (d_hot_cols_out)
+      LB_CUDA(cudaMemcpyAsync(d_hot_cols_out, A->hot_cols, (size_t)A->hot_n * 4, cudaMemcpyDeviceToDevice, S(stream)));
+    if (d_hot_col_idx_out)
+      LB_CUDA(cudaMemcpyAsync(d_hot_col_idx_out, A->hcol, (size_t)A->nnz * 4, cudaMemcpyDeviceToDevice, S(stream)));
+  }
   return LB_OK;
 }
 

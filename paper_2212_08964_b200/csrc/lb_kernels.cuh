@@ -103,12 +103,8 @@ __global__ void max_row_kernel(int rows, const int* __restrict__ off, int* out) 
 // k + off[k+1] is the merge position of row end k (row end before nonzero off[k+1], reading
 // R1); it is strictly increasing in k, so i is a lower-bound binary search on
 // [max(0, d-nnz), min(d, rows)] (below d-nnz every row end precedes d).
-__global__ void partition_kernel(int rows, int nnz, const int* __restrict__ off, int64_t L, int64_t T,
-                                 int2* __restrict__ coords) {
-  // PDL: let the dependent tile kernel start its prologue now (it waits for our completion)
-  asm volatile("griddepcontrol.launch_dependents;");
-  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (t > T) return;
+__device__ __forceinline__ int2 merge_path_search(int rows, int nnz, const int* __restrict__ off, int64_t t,
+                                                  int64_t L) {
   const int64_t total = (int64_t)rows + nnz;
   const int64_t d = t * L < total ? t * L : total;
   int lo = (int)(d - nnz > 0 ? d - nnz : 0);
@@ -118,7 +114,31 @@ __global__ void partition_kernel(int rows, int nnz, const int* __restrict__ off,
     if ((int64_t)mid + __ldg(off + mid + 1) < d) lo = mid + 1;
     else hi = mid;
   }
-  coords[t] = make_int2(lo, (int)(d - lo));
+  return make_int2(lo, (int)(d - lo));
+}
+
+__global__ void partition_kernel(int rows, int nnz, const int* __restrict__ off, int64_t L, int64_t T,
+                                 int2* __restrict__ coords) {
+  // PDL: let the dependent tile kernel start its prologue now (it waits for our completion)
+  asm volatile("griddepcontrol.launch_dependents;");
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t > T) return;
+  coords[t] = merge_path_search(rows, nnz, off, t, L);
+}
+
+// The same partition (threads 0..T; T = -1 skips it) fused with the per-call gather of a hot-column
+// plan's x values: threads T+1 .. T+hot_n write x_hot[h] = x[hot_cols[h]] (lb_csr_plan_hot_x).
+__global__ void partition_xhot_kernel(int rows, int nnz, const int* __restrict__ off, int64_t L, int64_t T,
+                                      int2* __restrict__ coords, const int* __restrict__ hot_cols, int hot_n,
+                                      const float* __restrict__ x, float* __restrict__ x_hot) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t <= T) {
+    coords[t] = merge_path_search(rows, nnz, off, t, L);
+    return;
+  }
+  const int64_t h = t - (T + 1);
+  if (h < hot_n) x_hot[h] = __ldg(x + __ldg(hot_cols + h));
 }
 
 // Nonzero-splitting partition (table; reading R19): tiles of L nonzeros, T = max(1,
@@ -410,6 +430,8 @@ struct PipeArgs {
   int* carry_row;
   float* carry_val;
   unsigned* ticket;  // zero before launch; the last CTA resets it
+  const float* x_hot;  // hot-column plan: x of the planned hot columns, gathered this call
+  int hot_n4;          // number of float4s of x_hot staged in shared memory (0: no plan)
 };
 
 // Tile length for E nonzeros per thread: the 16-byte-aligned nonzero range of a tile spans at
@@ -1050,19 +1072,27 @@ __device__ __forceinline__ void stream_load(const PipeArgs& a, int4 c, int k, in
   }
 }
 
+// One x value.  With a hot-column plan (HOT) the column stream holds ~slot (< 0) for planned hot
+// columns, whose x values sit in shared memory (sx); other columns are gathered from global x.
+template <bool XKEEP, bool HOT>
+__device__ __forceinline__ float gather_x(const PipeArgs& a, const float* sx, int c, uint64_t xpol) {
+  if (HOT && c < 0) return sx[~c];
+  return XKEEP ? ld_x_keep(a.x + c, xpol) : ld_x(a.x + c);
+}
+
 // gathers x for the round's valid positions; invalid positions get val = 0 (they add exactly 0)
-template <bool XKEEP>
+template <bool XKEEP, bool HOT = false>
 __device__ __forceinline__ void stream_gather(const PipeArgs& a, int4 c, int k, int lane, StreamRound& d,
-                                              float (&xv)[8], uint64_t xpol) {
+                                              float (&xv)[8], uint64_t xpol, const float* sx = nullptr) {
   const int q0 = 256 * k + 8 * lane, lo = c.y & 7, hi = c.w - (c.y & ~7);
   if (q0 >= lo && q0 + 8 <= hi) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) xv[e] = XKEEP ? ld_x_keep(a.x + d.col[e], xpol) : ld_x(a.x + d.col[e]);
+    for (int e = 0; e < 8; ++e) xv[e] = gather_x<XKEEP, HOT>(a, sx, d.col[e], xpol);
   } else {
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const bool ok = q0 + e >= lo && q0 + e < hi;
-      xv[e] = ok ? (XKEEP ? ld_x_keep(a.x + d.col[e], xpol) : ld_x(a.x + d.col[e])) : 0.f;
+      xv[e] = ok ? gather_x<XKEEP, HOT>(a, sx, d.col[e], xpol) : 0.f;
       if (!ok) d.val[e] = 0.f;
     }
   }
@@ -1132,12 +1162,16 @@ __device__ __forceinline__ void tail_clear8(unsigned* p) {
 
 // TailT: unsigned short for merge-path tiles (<= L rows), unsigned for nonzero-split tiles (any
 // number of rows per tile).
-template <int W, int R, int MINB, bool XKEEP, typename TailT = unsigned short>
+// HOT: the column stream is a hot-column plan's remapped copy (lb_csr_plan_hot_x); the CTA stages
+// the x values of the hot columns (a.x_hot, a.hot_n4 float4s) in dynamic shared memory and serves
+// those gathers from it -- one CTA per SM so the staged copy is shared by all of its warps.
+template <int W, int R, int MINB, bool XKEEP, typename TailT = unsigned short, bool HOT = false>
 __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) {
   using Cfg = StreamCfg<R>;
   constexpr int K = Cfg::K;
   __shared__ __align__(16) TailT s_tail[W][Cfg::kCap];
   __shared__ int s_last;
+  extern __shared__ __align__(16) float s_xhot[];
 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gw = blockIdx.x * W + warp;  // global warp id: owns tiles [t_begin, t_end)
@@ -1148,7 +1182,12 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
   TailT* tail = s_tail[warp];
   for (int w = lane; w < Cfg::kCap * (int)sizeof(TailT) / 16; w += 32)
     reinterpret_cast<uint4*>(tail)[w] = make_uint4(0u, 0u, 0u, 0u);
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: coords are read below
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: coords (and x_hot) are read below
+  if (HOT) {
+    for (int i = threadIdx.x; i < a.hot_n4; i += W * 32)
+      reinterpret_cast<float4*>(s_xhot)[i] = __ldcg(reinterpret_cast<const float4*>(a.x_hot) + i);
+    __syncthreads();
+  }
   __syncwarp();
 
   float rc = 0.f;  // partial sum of the row open at the current stream position (warp-uniform)
@@ -1169,14 +1208,14 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
     float x0[8], x1[8];
     stream_load(a, cT, 0, lane, d0, spol);
     if (1 < nsteps) stream_load(a, R > 1 ? cT : cT1, R > 1 ? 1 : 0, lane, d1, spol);
-    stream_gather<XKEEP>(a, cT, 0, lane, d0, x0, xpol);
+    stream_gather<XKEEP, HOT>(a, cT, 0, lane, d0, x0, xpol, s_xhot);
 
     int t = t_begin, k = 0;
     for (int st = 0; st < nsteps; ++st) {
       // (a) gathers for step st+1, loads for step st+2
       if (st + 1 < nsteps) {
         const bool same = k + 1 < R;
-        stream_gather<XKEEP>(a, same ? cT : cT1, same ? k + 1 : k + 1 - R, lane, d1, x1, xpol);
+        stream_gather<XKEEP, HOT>(a, same ? cT : cT1, same ? k + 1 : k + 1 - R, lane, d1, x1, xpol, s_xhot);
       }
       if (st + 2 < nsteps) {
         const int k2 = k + 2;
@@ -1291,6 +1330,160 @@ __global__ void __launch_bounds__(256) probe_stream_gather_kernel(int nnz, const
   }
   for (; i < nnz; ++i) s = fmaf(val[i], x[col[i]], s);
   if (flag) sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// ----------------------------------------------------------------------------- hot-column plan
+// B200 extension (not in the paper).  On random-column matrices the tile
+// processor is bound by x[col] gathers that miss L1 (~1 L1TEX line per clock per SM), while shared
+// memory serves random 4-byte reads several times faster.  A plan picks the `slots` columns with
+// the most stored entries (ties: lower column id first; only columns with >= 2 entries), assigns
+// them shared-memory slots, and rewrites a private copy of col_idx with ~slot for those entries.
+// Every call gathers x of the hot columns once (partition_xhot_kernel) and each CTA stages them in
+// shared memory.  Products and summation order are unchanged, so results are bitwise identical.
+
+// deg[c] = number of stored entries in column c (deg zeroed by the caller)
+__global__ void col_degree_kernel(int64_t nnz, const int* __restrict__ col, int* __restrict__ deg) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += stride)
+    atomicAdd(deg + __ldcs(col + k), 1);
+}
+
+// bins[b] += #{c : lo <= deg[c] < hi, (deg[c] - lo) / w == b}; block-private shared histogram
+constexpr int kDegBins = 8192;
+__global__ void __launch_bounds__(256) degree_hist_kernel(int cols, const int* __restrict__ deg, int64_t lo,
+                                                          int64_t hi, int64_t w, int* __restrict__ bins) {
+  __shared__ int h[kDegBins];
+  for (int i = threadIdx.x; i < kDegBins; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < cols; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t d = __ldg(deg + c);
+    if (d >= lo && d < hi) atomicAdd(&h[(d - lo) / w], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kDegBins; i += blockDim.x)
+    if (h[i]) atomicAdd(bins + i, h[i]);
+}
+
+// Slot assignment in column order.  Column c is hot if deg[c] >= t_hi ("above the threshold"), or
+// deg[c] == t_tie and it is among the first tie_budget such columns.  256 threads x 16 columns per
+// block; hot_count_kernel counts (above, tie) per block, hot_scan_kernel turns the counts into
+// exclusive offsets (one block), hot_assign_kernel writes slots.
+constexpr int kHotPer = 16;
+constexpr int kHotChunk = 256 * kHotPer;
+
+__device__ __forceinline__ int2 block_excl_scan2(int2 v, int2* total) {
+  __shared__ int2 ws[32];
+  __shared__ int2 wtot;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int a = v.x, b = v.y;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int ta = __shfl_up_sync(kFull, a, o), tb = __shfl_up_sync(kFull, b, o);
+    if (lane >= o) { a += ta; b += tb; }
+  }
+  if (lane == 31) ws[warp] = make_int2(a, b);
+  __syncthreads();
+  if (warp == 0) {
+    int2 w = lane < nw ? ws[lane] : make_int2(0, 0);
+    int wa = w.x, wb = w.y;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ta = __shfl_up_sync(kFull, wa, o), tb = __shfl_up_sync(kFull, wb, o);
+      if (lane >= o) { wa += ta; wb += tb; }
+    }
+    if (lane < nw) ws[lane] = make_int2(wa - w.x, wb - w.y);  // exclusive warp offsets
+    if (lane == nw - 1) wtot = make_int2(wa, wb);
+  }
+  __syncthreads();
+  const int2 base = ws[warp];
+  if (total) *total = wtot;
+  const int2 r = make_int2(base.x + a - v.x, base.y + b - v.y);
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(256) hot_count_kernel(int cols, const int* __restrict__ deg, int t_hi, int t_tie,
+                                                        int2* __restrict__ blk) {
+  const int64_t c0 = (int64_t)blockIdx.x * kHotChunk + (int64_t)threadIdx.x * kHotPer;
+  int a = 0, b = 0;
+#pragma unroll
+  for (int i = 0; i < kHotPer; ++i) {
+    if (c0 + i < cols) {
+      const int d = __ldg(deg + c0 + i);
+      a += d >= t_hi;
+      b += d == t_tie;
+    }
+  }
+  int2 tot;
+  block_excl_scan2(make_int2(a, b), &tot);
+  if (threadIdx.x == 0) blk[blockIdx.x] = tot;
+}
+
+// one block: blk[0..n) counts -> exclusive offsets; totals[0..1] = sums
+__global__ void __launch_bounds__(1024) hot_scan_kernel(int n, int2* __restrict__ blk, int* __restrict__ totals) {
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  const int b0 = threadIdx.x * per;
+  int a = 0, b = 0;
+  for (int i = 0; i < per; ++i)
+    if (b0 + i < n) { a += blk[b0 + i].x; b += blk[b0 + i].y; }
+  int2 tot;
+  const int2 ex = block_excl_scan2(make_int2(a, b), &tot);
+  int ra = ex.x, rb = ex.y;
+  for (int i = 0; i < per; ++i)
+    if (b0 + i < n) {
+      const int2 v = blk[b0 + i];
+      blk[b0 + i] = make_int2(ra, rb);
+      ra += v.x;
+      rb += v.y;
+    }
+  if (threadIdx.x == 0) { totals[0] = tot.x; totals[1] = tot.y; }
+}
+
+// deg_smap: in deg[c], out slot of c (-1: not hot); hot_cols[slot] = c; hot_nnz += deg of hot columns
+__global__ void __launch_bounds__(256) hot_assign_kernel(int cols, int* __restrict__ deg_smap, int t_hi, int t_tie,
+                                                         int n_above, int tie_budget, const int2* __restrict__ blk,
+                                                         int* __restrict__ hot_cols,
+                                                         unsigned long long* __restrict__ hot_nnz) {
+  const int64_t c0 = (int64_t)blockIdx.x * kHotChunk + (int64_t)threadIdx.x * kHotPer;
+  int d[kHotPer];
+  int a = 0, b = 0;
+#pragma unroll
+  for (int i = 0; i < kHotPer; ++i) {
+    d[i] = c0 + i < cols ? deg_smap[c0 + i] : 0;
+    a += d[i] >= t_hi;
+    b += d[i] == t_tie;
+  }
+  const int2 ex = block_excl_scan2(make_int2(a, b), nullptr);
+  int ra = blk[blockIdx.x].x + ex.x, rb = blk[blockIdx.x].y + ex.y;
+  unsigned long long sum = 0;
+#pragma unroll
+  for (int i = 0; i < kHotPer; ++i) {
+    if (c0 + i >= cols) break;
+    int slot = -1;
+    if (d[i] >= t_hi) slot = ra++;
+    else if (d[i] == t_tie) {
+      if (rb < tie_budget) slot = n_above + rb;
+      ++rb;
+    }
+    if (slot >= 0) {
+      hot_cols[slot] = (int)(c0 + i);
+      sum += (unsigned)d[i];
+    }
+    deg_smap[c0 + i] = slot;
+  }
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+  if ((threadIdx.x & 31) == 0 && sum) atomicAdd(hot_nnz, sum);
+}
+
+// hcol[k] = ~slot if col[k] is hot, else col[k]
+__global__ void hot_remap_kernel(int64_t nnz, const int* __restrict__ col, const int* __restrict__ smap,
+                                 int* __restrict__ hcol) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += stride) {
+    const int c = __ldcs(col + k);
+    const int sl = __ldg(smap + c);
+    hcol[k] = sl >= 0 ? ~sl : c;
+  }
 }
 
 // ----------------------------------------------------------------------------- SpMM (NEXT-2)

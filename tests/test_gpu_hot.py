@@ -1,0 +1,144 @@
+"""GPU parity of the hot-column plan (lb_csr_plan_hot_x) through the C ABI.
+
+* the plan (slot table and remapped column stream) is integer work: bit-exact against
+  oracle.hot_columns (small matrices) or against the test-side sort derivation pinned to the oracle
+  in tests/test_oracle_pins.py (full BASELINE.json sizes);
+* y with the plan: bit-exact vs the oracle in integer mode, within 1e-5 * s + 1e-30 in float mode,
+  and bitwise identical to the merge-path call without a plan (same products, same order).
+"""
+import numpy as np
+import pytest
+import torch
+
+import lbgen
+import oracle
+import paper_2212_08964_b200 as lb
+from test_gpu_parity import SMALL, _csr, _packed, _sample_rows, check_y, random_csr, ref
+from test_oracle_pins import hot_columns_by_sort, hot_slot_table_by_sort
+
+pytestmark = pytest.mark.gpu
+
+
+def _plan_matches(M: lb.CsrMatrix, A: lbgen.Csr, slots: int, ref_fn):
+    n, hn = M.plan_hot_x(slots)
+    sc, rm, hn_ref = ref_fn(A.col_idx.cpu().numpy(), A.cols, slots)
+    assert n == sc.size and hn == hn_ref, (n, sc.size, hn, hn_ref)
+    if n:
+        hot, hcol = M.hot_plan()
+        assert np.array_equal(hot.cpu().numpy(), sc), "slot table"
+        assert np.array_equal(hcol.cpu().numpy(), rm), "remapped column stream"
+    return n
+
+
+@pytest.mark.parametrize("slots", [1, 5, 333, 4096, 32768, 45056])
+@pytest.mark.parametrize("name", ["rmat12", "rmat14", "skewed", "c1", "stencil100", "uniform_rows"])
+def test_plan_bit_exact(name, slots):
+    A = SMALL[name]("int")
+    M = lb.CsrMatrix.from_csr(A)
+    fn = oracle.hot_columns if A.cols * min(slots, A.cols) <= 2e8 else hot_columns_by_sort
+    _plan_matches(M, A, slots, fn)
+
+
+@pytest.mark.parametrize("L", [504, 1016])
+@pytest.mark.parametrize("vmode", ["int", "float"])
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_spmv_with_plan(name, vmode, L):
+    A = SMALL[name](vmode)
+    x = lbgen.make_x(A.cols, vmode, 21)
+    y_ref, s_ref = ref(A, x)
+    M = lb.CsrMatrix.from_csr(A)
+    M.set_items_per_tile(L)
+    xd = x.cuda()
+    y0 = M.spmv(xd, schedule="merge_path", repartition=True).clone()
+    for slots in (7, 2048, 0):
+        n, _ = M.plan_hot_x(slots)
+        assert n > 0 or name == "stencil100"
+        y = torch.full((A.rows,), float("nan"), device="cuda")
+        M.spmv(xd, y, "merge_path", repartition=True)
+        torch.cuda.synchronize()
+        check_y(y, y_ref, s_ref, vmode == "int", f"{name}/{vmode}/L{L}/slots{slots}")
+        assert torch.equal(y, y0), "plan changed the bits of y"
+        y.fill_(float("nan"))
+        M.spmv(xd, y, "merge_path")  # cached partition: x_hot gather alone before the tile kernel
+        torch.cuda.synchronize()
+        assert torch.equal(y, y0)
+
+
+@pytest.mark.parametrize("W", ["8", "16", "20"])
+def test_plan_kernel_widths(W, monkeypatch):
+    monkeypatch.setenv("LB_HOT_W", W)
+    rng = np.random.default_rng(int(W))
+    for trial in range(8):
+        A = random_csr(rng, int(rng.integers(1, 4000)), int(rng.integers(1, 700)), int(rng.integers(0, 80)),
+                       float(rng.random()) * 0.6, "int")
+        x = lbgen.make_x(A.cols, "int", trial)
+        y_ref, s_ref = ref(A, x)
+        M = lb.CsrMatrix.from_csr(A)
+        M.plan_hot_x(int(rng.integers(1, 600)))
+        for L in (504, 1016):
+            M.set_items_per_tile(L)
+            check_y(M.spmv(x.cuda(), schedule="merge_path"), y_ref, s_ref, True, f"W{W}/trial{trial}/L{L}")
+
+
+def test_plan_edge_cases():
+    # x changes between calls: the hot x values are re-gathered every call
+    A = lbgen.rmat(12, 16, 3, "int")
+    M = lb.CsrMatrix.from_csr(A)
+    assert M.plan_hot_x(1000)[0] == 1000
+    for seed in range(3):
+        x = lbgen.make_x(A.cols, "int", 100 + seed)
+        y_ref, s_ref = ref(A, x)
+        check_y(M.spmv(x.cuda(), schedule="merge_path"), y_ref, s_ref, True, f"x seed {seed}")
+    # drop the plan
+    assert M.plan_hot_x(-1) == (0, 0)
+    assert M.hot_plan() is None
+    assert "hot" not in M.kernel_name("merge_path")
+    # no column with two entries: no plan is kept
+    D = _csr(list(range(0, 1001)), 1000, col=list(range(1000)))
+    MD = lb.CsrMatrix.from_csr(D)
+    assert MD.plan_hot_x(0) == (0, 0)
+    # one giant row, every column hot
+    G = _csr([0, 50_000], 64, col=list(np.arange(50_000) % 64))
+    MG = lb.CsrMatrix.from_csr(G)
+    assert MG.plan_hot_x(0)[0] == 64
+    x = lbgen.make_x(64, "int", 5)
+    y_ref, s_ref = ref(G, x)
+    check_y(MG.spmv(x.cuda(), schedule="merge_path"), y_ref, s_ref, True, "giant row")
+    with pytest.raises(lb.LbError):
+        M.plan_hot_x(10 ** 6)
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4", "c5"])
+def test_plan_full_size(cfg):
+    """The plan at BASELINE.json sizes with the default slot budget (what bench.py times): slot table
+    and remapped stream bit-exact vs the sort derivation; y bitwise equal to the plan-less
+    merge path on every row and within tolerance of the oracle on sampled rows."""
+    torch.cuda.empty_cache()
+    A = lbgen.make_config(cfg, "float", device="cuda")
+    x = lbgen.x_for_config(cfg, A.cols, "float", device="cuda")
+    M = lb.CsrMatrix.from_csr(A, device="cuda")
+    y0 = M.spmv(x, schedule="merge_path", repartition=True).clone()
+    n, hn = M.plan_hot_x(0)
+    # slot table by the sort derivation (degrees by torch.bincount, test-side), remapped stream
+    # checked on the device by decoding it through the table
+    deg = torch.bincount(A.col_idx.long(), minlength=A.cols).cpu().numpy()
+    sc = hot_slot_table_by_sort(deg, 32768)
+    assert n == sc.size and hn == int(deg[sc].sum())
+    hot, hcol = M.hot_plan()
+    assert np.array_equal(hot.cpu().numpy(), sc)
+    is_hot = torch.zeros(A.cols, dtype=torch.bool, device="cuda")
+    is_hot[hot.long()] = True
+    neg = hcol < 0
+    assert torch.equal(neg, is_hot[A.col_idx.long()])
+    dec = torch.where(neg, hot[(~hcol).clamp(min=0).long()], hcol)
+    assert torch.equal(dec, A.col_idx)
+    del hcol, dec, neg
+    y = torch.full((A.rows,), float("nan"), device="cuda")
+    M.spmv(x, y, "merge_path", repartition=True)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y0)
+    coords = M.partition().cpu().numpy()
+    sel = _sample_rows(A, coords, 20_000, 3)
+    so, scol, sv = _packed(A, sel)
+    y_ref, s_ref = oracle.spmv_packed(so, scol, sv, x.cpu())
+    check_y(y[torch.as_tensor(sel, device="cuda")], y_ref, s_ref, False, f"{cfg}/plan")

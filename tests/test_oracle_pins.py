@@ -367,3 +367,67 @@ def test_partition_nz_worked_example_and_merge_path_points():
             # i_t (0 < t < T) is the closed-form count #{r : off[r+1] <= j_t}
             for t in range(1, c.shape[0] - 1):
                 assert i[t] == np.count_nonzero(off[1:] <= j[t])
+
+
+# ---------------------------------------------------------------- hot-column plan
+
+HOT_GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "hot_columns_examples.json")
+
+
+def hot_slot_table_by_sort(deg: np.ndarray, slots: int) -> np.ndarray:
+    """Slot table of the plan from column degrees: lexsort (the oracle uses repeated maximum search)."""
+    cand = np.nonzero(deg >= 2)[0]
+    if cand.size < slots:
+        return cand.astype(np.int32)
+    order = np.lexsort((cand, -deg[cand]))  # deg descending, then column ascending
+    hot = np.sort(cand[order[:slots]])
+    tau = deg[hot].min()
+    return np.concatenate([hot[deg[hot] > tau], hot[deg[hot] == tau]]).astype(np.int32)
+
+
+def hot_columns_by_sort(col: np.ndarray, cols: int, slots: int):
+    """Independent derivation of the plan: bincount + lexsort."""
+    deg = np.bincount(col, minlength=cols).astype(np.int64) if col.size else np.zeros(cols, np.int64)
+    slot_cols = hot_slot_table_by_sort(deg, slots)
+    slot_of = np.full(cols, -1, np.int64)
+    slot_of[slot_cols] = np.arange(slot_cols.size)
+    s = slot_of[col] if col.size else np.zeros(0, np.int64)
+    remapped = np.where(s >= 0, ~s, col).astype(np.int32)
+    return slot_cols.astype(np.int32), remapped, int(deg[slot_cols].sum())
+
+
+def test_hot_columns_worked_examples():
+    g = json.load(open(HOT_GOLDEN))
+    col = np.array(g["col_idx"], np.int32)
+    for case in g["cases"]:
+        sc, rm, hn = oracle.hot_columns(col, g["cols"], case["slots"])
+        assert sc.tolist() == case["slot_cols"], case
+        assert hn == case["hot_nnz"], case
+        slot_of = {c: i for i, c in enumerate(case["slot_cols"])}
+        assert rm.tolist() == [~slot_of[c] if c in slot_of else c for c in g["col_idx"]]
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_hot_columns_match_sort_derivation(seed):
+    rng = np.random.default_rng(seed)
+    cols = int(rng.integers(1, 400))
+    nnz = int(rng.integers(0, 3000))
+    # skewed column popularity (power-law-ish) with many ties
+    w = rng.pareto(1.2, cols) + 0.05
+    col = rng.choice(cols, size=nnz, p=w / w.sum()).astype(np.int32)
+    for slots in (1, 2, 7, int(rng.integers(1, cols + 5)), cols + 10):
+        sc, rm, hn = oracle.hot_columns(col, cols, slots)
+        sc2, rm2, hn2 = hot_columns_by_sort(col, cols, slots)
+        assert np.array_equal(sc, sc2), (seed, slots)
+        assert np.array_equal(rm, rm2), (seed, slots)
+        assert hn == hn2
+        # invariants: every hot column is at least as popular as every non-hot candidate; decoding
+        # the remapped stream through the slot table gives col_idx back
+        deg = np.bincount(col, minlength=cols)
+        hot = np.zeros(cols, bool)
+        hot[sc] = True
+        if (~hot & (deg >= 2)).any() and sc.size:
+            assert deg[sc].min() >= deg[~hot & (deg >= 2)].max()
+        dec = np.where(rm < 0, sc[np.where(rm < 0, ~rm, 0)] if sc.size else 0, rm)
+        assert np.array_equal(dec, col)
+        assert sc.size == min(slots, int((deg >= 2).sum()))
