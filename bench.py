@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="budget for the cpu_baseline sample")
     ap.add_argument("--multi", action="store_true", help="use the multi-GPU step even at world size 1 (testing)")
+    ap.add_argument("--hot-slots", type=int, default=0,
+                    help="hot-column plan (lb_csr_plan_hot_x) slot budget: 0 = library default, -1 = no plan")
     return ap.parse_args()
 
 
@@ -210,6 +212,32 @@ def run_single(args, cfg):
     def step():
         M.spmv(x, y, sched, repartition=True)
 
+    # the plain-CSR rate first (no plan), then the per-matrix hot-column plan the timed steps use
+    no_plan = None
+    plan = None
+    if args.hot_slots >= 0 and sched == "merge_path":
+        for _ in range(3):
+            step()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_np = max(10, min(args.steps, 200))
+        ea.record(stream)
+        for _ in range(n_np):
+            step()
+        eb.record(stream)
+        torch.cuda.synchronize()
+        ms_np = ea.elapsed_time(eb) / n_np
+        no_plan = {"value": round(nnz / (ms_np * 1e-3) / 1e9, 3), "ms_per_step": round(ms_np, 5),
+                   "kernel": M.kernel_name(sched), "steps": n_np}
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        hot_n, hot_nnz = M.plan_hot_x(args.hot_slots)
+        torch.cuda.synchronize()
+        build_ms = (time.perf_counter() - t0) * 1e3
+        plan = {"kind": "hot-column plan (lb_csr_plan_hot_x, DESIGN.md 6b)", "slots_requested": args.hot_slots,
+                "hot_cols": hot_n, "hot_nnz_frac": round(hot_nnz / max(nnz, 1), 4),
+                "build_ms": round(build_ms, 2), "built": "once per matrix, before the timed region",
+                "break_even_steps": None}
+
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
@@ -251,8 +279,11 @@ def run_single(args, cfg):
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (lbgen counter-hash generator, seeded)",
         "config": {"workload": cfg, "desc": lbgen.CONFIG_DESC.get(cfg, cfg), "rows": rows, "cols": cols, "nnz": nnz,
                    "schedule": sched, "items_per_tile": args.items_per_tile, "parallelism": "1 GPU",
-                   "values": "uniform [-1,1) fp32", "step": "lb_spmv_ex(REPARTITION): partition + tiles + fixup",
+                   "values": "uniform [-1,1) fp32", "step": "lb_spmv_ex(REPARTITION): partition" + (" + hot x gather" if plan and plan["hot_cols"] else "")
+                   + " + tiles + fixup",
                    "l2": "inputs (%.2f GB) larger than the 126 MB L2; no flush between steps" % (alg / 1e9)},
+        "plan": plan,
+        "no_plan": no_plan,
         "gpu_launches": int(launches),
         "phase_ms": {"partition": round(float(ph[0]), 5), "main": round(main_ms, 5), "fixup": round(float(ph[2]), 5)},
         "roofline": {"bound": "hbm", "kernel": M.kernel_name(sched),
@@ -272,6 +303,8 @@ def run_single(args, cfg):
             "peak_source": "lb_probe_stream_gather: same col/val/x, 256-bit stream loads + gathers, no rows"}
     except Exception as e:  # pragma: no cover
         rec["roofline_gather"] = {"error": str(e)}
+    if plan is not None and no_plan is not None and ms < no_plan["ms_per_step"]:
+        plan["break_even_steps"] = int(np.ceil(plan["build_ms"] / (no_plan["ms_per_step"] - ms)))
     if args.no_extras:
         print(json.dumps(rec))
         return
@@ -368,7 +401,9 @@ def run_multi(args, cfg):
                        "schedule": args.schedule, "parallelism": f"row shards x{world} (equal nnz), NCCL all-gather of y",
                        "step": "lb_spmv_multi: shard SpMV + all-gather(v) of y",
                        "l2": "inputs larger than L2; no flush"},
-            "gpu_launches": int(launches),
+            "plan": plan,
+        "no_plan": no_plan,
+        "gpu_launches": int(launches),
             "spmv_only": {"value": round(nnz / (spmv_ms * 1e-3) / 1e9, 3), "unit": "GNZ/s", "ms": round(spmv_ms, 5)},
             "e2e": None,
         }

@@ -1073,29 +1073,34 @@ __device__ __forceinline__ void stream_load(const PipeArgs& a, int4 c, int k, in
 }
 
 // One x value.  With a hot-column plan (HOT) the column stream holds ~slot (< 0) for planned hot
-// columns, whose x values sit in shared memory (sx); other columns are gathered from global x.
+// columns, whose x values sit in shared memory at byte address sxb + 4*slot; other columns are
+// gathered from global x.  One predicated LDS and one predicated LDG, no branch.
 template <bool XKEEP, bool HOT>
-__device__ __forceinline__ float gather_x(const PipeArgs& a, const float* sx, int c, uint64_t xpol) {
-  if (HOT && c < 0) return sx[~c];
-  return XKEEP ? ld_x_keep(a.x + c, xpol) : ld_x(a.x + c);
+__device__ __forceinline__ float gx(const float* __restrict__ x, uint32_t sxb, int c, uint64_t xpol) {
+  if (HOT) {
+    float v;
+    asm("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, 0;\n\t@p ld.shared.f32 %0, [%2];\n\t"
+        "@!p ld.global.nc.f32 %0, [%3];\n\t}"
+        : "=f"(v)
+        : "r"(c), "r"(sxb + ((unsigned)~c << 2)), "l"(x + c));
+    return v;
+  }
+  return XKEEP ? ld_x_keep(x + c, xpol) : ld_x(x + c);
 }
 
-// gathers x for the round's valid positions; invalid positions get val = 0 (they add exactly 0)
-template <bool XKEEP, bool HOT = false>
-__device__ __forceinline__ void stream_gather(const PipeArgs& a, int4 c, int k, int lane, StreamRound& d,
-                                              float (&xv)[8], uint64_t xpol, const float* sx = nullptr) {
-  const int q0 = 256 * k + 8 * lane, lo = c.y & 7, hi = c.w - (c.y & ~7);
-  if (q0 >= lo && q0 + 8 <= hi) {
+// the 8 gathers of a lane's round (every loaded column index is valid; positions outside the tile
+// are masked later by zeroing their values)
+template <bool XKEEP, bool HOT>
+__device__ __forceinline__ void gx8(const float* __restrict__ x, uint32_t sxb, const StreamRound& d, float (&xv)[8],
+                                    uint64_t xpol) {
 #pragma unroll
-    for (int e = 0; e < 8; ++e) xv[e] = gather_x<XKEEP, HOT>(a, sx, d.col[e], xpol);
-  } else {
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const bool ok = q0 + e >= lo && q0 + e < hi;
-      xv[e] = ok ? gather_x<XKEEP, HOT>(a, sx, d.col[e], xpol) : 0.f;
-      if (!ok) d.val[e] = 0.f;
-    }
-  }
+  for (int e = 0; e < 8; ++e) xv[e] = gx<XKEEP, HOT>(x, sxb, d.col[e], xpol);
+}
+
+// y store predicated on `p` (no branch)
+__device__ __forceinline__ void st_cs_if(float* ptr, float v, bool p) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q st.global.cs.f32 [%0], %1;\n\t}"
+               :: "l"(ptr), "f"(v), "r"((unsigned)p) : "memory");
 }
 
 template <int R, int K>
@@ -1193,6 +1198,8 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
   float rc = 0.f;  // partial sum of the row open at the current stream position (warp-uniform)
   int i_last = t_begin < t_end ? __ldg(&a.coords[t_end].x) : a.rows;
   if (t_begin < t_end) {
+    const float* __restrict__ xg = a.x;
+    const uint32_t sxb = HOT ? (uint32_t)__cvta_generic_to_shared(s_xhot) : 0u;
     const int nsteps = (t_end - t_begin) * R;
     // coordinates of tiles t, t+1, t+2 (int4 = i0, j0, i1, j1)
     int4 cT = tile_coords(a, t_begin);
@@ -1203,24 +1210,22 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
     bool r0e = stream_row_pass<R, K, TailT>(a, cT, lane, olo, ohi, tail);
     if (t_begin + 1 < t_end) stream_prefetch_offsets<R, K>(a, cT1, lane, olo, ohi);
     __syncwarp();
-    // pipeline registers: step s (gathered), s+1 (gathered next), s+2 (loading)
-    StreamRound d0, d1, d2;
-    float x0[8], x1[8];
-    stream_load(a, cT, 0, lane, d0, spol);
-    if (1 < nsteps) stream_load(a, R > 1 ? cT : cT1, R > 1 ? 1 : 0, lane, d1, spol);
-    stream_gather<XKEEP, HOT>(a, cT, 0, lane, d0, x0, xpol, s_xhot);
+    // three rounds in flight: reduced (gathered), gathering, loading -- rotated by unrolling the
+    // loop three times, so no register is copied between rounds
+    StreamRound D0, D1, D2;
+    float X0[8], X1[8], X2[8];
+    stream_load(a, cT, 0, lane, D0, spol);
+    if (1 < nsteps) stream_load(a, R > 1 ? cT : cT1, R > 1 ? 1 : 0, lane, D1, spol);
+    gx8<XKEEP, HOT>(xg, sxb, D0, X0, xpol);
 
-    int t = t_begin, k = 0;
-    for (int st = 0; st < nsteps; ++st) {
-      // (a) gathers for step st+1, loads for step st+2
-      if (st + 1 < nsteps) {
-        const bool same = k + 1 < R;
-        stream_gather<XKEEP, HOT>(a, same ? cT : cT1, same ? k + 1 : k + 1 - R, lane, d1, x1, xpol, s_xhot);
-      }
+    int t = t_begin, k = 0, st = 0;
+    auto step = [&](StreamRound& dc, float (&xc)[8], StreamRound& dn, float (&xn)[8], StreamRound& dl) {
+      // (a) gathers for round st+1, loads for round st+2
+      if (st + 1 < nsteps) gx8<XKEEP, HOT>(xg, sxb, dn, xn, xpol);
       if (st + 2 < nsteps) {
         const int k2 = k + 2;
         const bool same = k2 < R;
-        stream_load(a, same ? cT : cT1, same ? k2 : k2 - R, lane, d2, spol);
+        stream_load(a, same ? cT : cT1, same ? k2 : k2 - R, lane, dl, spol);
       }
       // (b) the row open at the tile start has no nonzero here: it ends now with the carry
       const int i0 = cT.x;
@@ -1228,41 +1233,55 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
         if (lane == 0) __stcs(a.y + i0, rc);
         rc = 0.f;
       }
-      // (c) reduce this round
-      unsigned rids[8];
-      tail_read8(&tail[256 * k + 8 * lane], rids);
-      unsigned any = 0u;
-      float run = 0.f, first_val = 0.f;
-      int first_r = -1;
+      // (c) positions outside the tile's nonzero range [lo, hi) add exactly zero (warp-uniform test)
+      {
+        const int lo = cT.y & 7, hi = cT.w - (cT.y & ~7);
+        if ((k == 0 && lo) || 256 * k + 256 > hi) {
+          const int q0 = 256 * k + 8 * lane;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        run = fmaf(d0.val[e], x0[e], run);
-        const unsigned rid = rids[e];
-        any |= rid;
-        if (rid) {
-          const int r = (int)rid - 1;
-          if (first_r < 0) { first_r = r; first_val = run; }
-          else __stcs(a.y + i0 + r, run);  // row started inside this lane's 8 nonzeros
-          run = 0.f;
+          for (int e = 0; e < 8; ++e)
+            if (q0 + e < lo || q0 + e >= hi) dc.val[e] = 0.f;
         }
       }
-      bool f = first_r >= 0;
+      // (d) reduce this round: rows that end inside the lane's 8 nonzeros after its first row end
+      // are complete; the first one waits for the carry-in from the lanes before
+      unsigned rids[8];
+      tail_read8(&tail[256 * k + 8 * lane], rids);
+      float* yt = a.y + i0 - 1;  // row r of the tile ends where rid = r + 1
+      unsigned any = 0u, first_rid = 0u;
+      float run = 0.f, first_val = 0.f;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        run = fmaf(dc.val[e], xc[e], run);
+        const unsigned rid = rids[e];
+        any |= rid;
+        st_cs_if(yt + rid, run, rid != 0u && first_rid != 0u);
+        const bool take = rid != 0u && first_rid == 0u;
+        first_val = take ? run : first_val;
+        first_rid = take ? rid : first_rid;
+        run = rid != 0u ? 0.f : run;
+      }
+      // segmented inclusive scan over the lanes (Kogge-Stone; a lane with a row end starts a new
+      // segment): lane l adds the partial of lane l-o unless a lane in (l-o, l] has a row end
+      const unsigned B = __ballot_sync(kFull, first_rid != 0u);
       float v = run;
-      warp_segscan_incl(f, v, (unsigned)lane);
-      float lval = __shfl_up_sync(kFull, v, 1);
-      const int lf = __shfl_up_sync(kFull, (int)f, 1);
-      const int agg_f = __shfl_sync(kFull, (int)f, 31);
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const float vo = __shfl_up_sync(kFull, v, o);
+        const bool reset = lane >= o ? ((B >> (lane - o + 1)) & ((1u << o) - 1u)) != 0u : true;
+        if (!reset) v = vo + v;
+      }
+      const float lval = __shfl_up_sync(kFull, v, 1);
       const float agg_v = __shfl_sync(kFull, v, 31);
-      if (first_r >= 0) {
+      if (first_rid != 0u) {
+        const bool lf = (B & ((1u << lane) - 1u)) != 0u;  // a row ended in an earlier lane
         const float carry_in = lane == 0 ? rc : (lf ? lval : rc + lval);
-        __stcs(a.y + i0 + first_r, carry_in + first_val);
+        __stcs(yt + first_rid, carry_in + first_val);
       }
       if (any) tail_clear8(&tail[256 * k + 8 * lane]);
-      rc = agg_f ? agg_v : rc + agg_v;
-      // (d) rotate the pipeline
-#pragma unroll
-      for (int e = 0; e < 8; ++e) { d0.val[e] = d1.val[e]; x0[e] = x1[e]; d1.col[e] = d2.col[e]; d1.val[e] = d2.val[e]; }
-      if (++k == R) {  // tile t done: row pass of tile t+1 (offsets prefetched), advance coords
+      rc = B ? agg_v : rc + agg_v;
+      // (e) tile t done: row pass of tile t+1 (offsets prefetched), advance coords
+      if (++k == R) {
         k = 0;
         ++t;
         __syncwarp();
@@ -1275,6 +1294,14 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
         }
       }
       __syncwarp();
+    };
+    while (true) {
+      step(D0, X0, D1, X1, D2);
+      if (++st == nsteps) break;
+      step(D1, X1, D2, X2, D0);
+      if (++st == nsteps) break;
+      step(D2, X2, D0, X0, D1);
+      if (++st == nsteps) break;
     }
   }
 

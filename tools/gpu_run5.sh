@@ -1,0 +1,5 @@
+export LB_HOT_W=16
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:merge_stream -s 2 -c 1 -o gpurun_out/prof_c3_hot16k_v2 python tools/prof_run.py c3 16384 4 > gpurun_out/ncu_hot.log 2>&1; echo "ncu hot rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:merge_stream -s 2 -c 1 -o gpurun_out/prof_c3_base_v2 python tools/prof_run.py c3 -1 4 > gpurun_out/ncu_base.log 2>&1; echo "ncu base rc=$?"
+unset LB_HOT_W
+timeout 600 python bench.py --hot-slots 16384 > gpurun_out/bench_hot.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench_hot.log
