@@ -68,14 +68,14 @@ def compulsory_bytes(rows, cols, nnz):
     return 8 * nnz + 4 * (rows + 1) + 4 * rows + 4 * cols
 
 
-def ncu_traffic(cfg, sched, L, kernel):
+def ncu_traffic(cfg, sched, L, kernel, hot_slots=None):
     """DRAM bytes per launch of this kernel from a committed ncu --set full capture (or None)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    e = d.get(f"{cfg}/{sched}/L{L}")
+    e = d.get(f"{cfg}/{sched}/L{L}" + (f"/hot{hot_slots}" if hot_slots else ""))
     if e is None or e.get("kernel") != kernel.split(" ")[0]:
         return None
     return e.get("dram_bytes_per_launch")
@@ -288,7 +288,8 @@ def run_single(args, cfg):
         "phase_ms": {"partition": round(float(ph[0]), 5), "main": round(main_ms, 5), "fixup": round(float(ph[2]), 5)},
         "roofline": {"bound": "hbm", "kernel": M.kernel_name(sched),
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
-                     "traffic": ncu_traffic(cfg, sched, args.items_per_tile, M.kernel_name(sched)),
+                     "traffic": ncu_traffic(cfg, sched, args.items_per_tile, M.kernel_name(sched),
+                                          plan["hot_cols"] if plan and plan["hot_cols"] else None),
                      "algorithmic_bytes": alg,
                      "peak_source": peak_src,
                      "kernel_ms_from": "mean of 20 lb_spmv_phase_times calls (CUDA events on the launch stream)"},

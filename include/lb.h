@@ -187,7 +187,7 @@ lb_status_t lb_spmm(lb_csr_t A, int64_t n, const float* d_X, int64_t ldx, float*
  * each CTA stages them in shared memory, and the tile kernel reads hot x values from there.  The
  * products and the summation order are unchanged: y is bitwise identical to the call without a
  * plan.  Other schedules ignore the plan.
- *  slots          0 = default (32768: 128 KB of shared memory per SM); 1 .. 45056; < 0 drops the plan.
+ *  slots          0 = default (16384: 64 KB of shared memory per SM); 1 .. 45056; < 0 drops the plan.
  *  hot_cols_out   (optional) number of planned hot columns (0: no plan was kept).
  *  hot_nnz_out    (optional) number of stored entries in hot columns.
  * Cost: device memory 4*nnz + 8*hot + 4*cols (temporary); a degree histogram, 1-4 selection passes

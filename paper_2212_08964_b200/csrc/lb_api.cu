@@ -518,7 +518,7 @@ lb_status_t launch_nz_tiles(lb_csr_s* A, const float* x, float* y, stream_t s) {
 // Tile kernel with the plan: warp-streamed, one CTA of W warps per SM, x of the hot columns staged
 // in dynamic shared memory.  W and the slot budget were chosen by measurement;
 // LB_HOT_W overrides W (8, 16, 20) for sweeps.
-constexpr int kHotSlotsDefault = 32768;  // 128 KB of shared memory per SM
+constexpr int kHotSlotsDefault = 16384;  // 64 KB of shared memory per SM (best measured on C3)
 constexpr int kHotSlotsMax = 45056;      // 176 KB
 constexpr int kHotDynMax = kHotSlotsMax * 4;
 
