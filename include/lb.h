@@ -172,37 +172,49 @@ lb_status_t lb_select_schedule(lb_csr_t A, void* stream, lb_schedule_t* out);
 lb_status_t lb_spmm(lb_csr_t A, int64_t n, const float* d_X, int64_t ldx, float* d_Y, int64_t ldy, void* stream);
 
 /*
- * lb_csr_plan_hot_x -- hot-column plan for MERGE_PATH (B200 extension; not in the paper -- DESIGN.md
+ * lb_csr_plan_hot_x -- x-reuse plan for MERGE_PATH (B200 extension; not in the paper -- DESIGN.md
  * section 6b).  Background: a merge-path tile reads col/val as a stream but x[col] as random 4-byte
- * gathers (Listing 3 P:980 `x[column_indices[nz]]`), and on B200 gathers that miss L1 are served at
- * about one L1TEX line per clock per SM, while shared memory serves random reads several times
- * faster.  The plan:
- *   deg(c)   = number of stored entries in column c; candidates = columns with deg(c) >= 2;
- *   fewer than `slots` candidates: all are hot, slots numbered in ascending column order;
- *   otherwise: the hot set is the first `slots` candidates ordered by (deg descending, column
- *              ascending); with tau = the smallest degree in it, slots go first to the hot
- *              columns with deg > tau, then to those with deg == tau, each in ascending column order;
- *   a private copy of col_idx in which every entry of a hot column c holds ~slot(c) (< 0).
- * With a plan, every lb_spmv(MERGE_PATH) call (L = 504 or 1016) gathers x of the hot columns once,
- * each CTA stages them in shared memory, and the tile kernel reads hot x values from there.  The
- * products and the summation order are unchanged: y is bitwise identical to the call without a
- * plan.  Other schedules ignore the plan.
+ * gathers (Listing 3 P:980 `x[column_indices[nz]]`).  On B200 every gather that misses L1 costs a
+ * 32-byte L2 sector and an L1TEX wavefront, and when x exceeds the L2 a DRAM sector too, while
+ * shared memory serves random 4-byte reads several times faster.  The plan orders the columns by
+ *   deg(c) = number of stored entries in column c  (candidates: deg(c) >= 2)
+ * and builds two tiers:
+ *  HOT   fewer than `slots` candidates: all are hot, slots numbered in ascending column order;
+ *        otherwise the first `slots` candidates ordered by (deg descending, column ascending); with
+ *        tau1 = the smallest degree among them, slots go first to the hot columns with deg > tau1,
+ *        then to those with deg == tau1, each in ascending column order.
+ *  WARM  (only when the hot tier is full and warm_cols > 0) the non-hot columns with
+ *        deg >= tau2, where tau2 is the smallest degree >= 2 with #{deg >= tau2} <= slots +
+ *        warm_cols (whole degree levels; warm_cols is an upper bound), provided tau2 <= tau1;
+ *        numbered in ascending column order.
+ * and a private copy of col_idx in which an entry of hot column c holds ~slot(c) (< 0), an entry
+ * of warm column c holds cols + warm_index(c), other entries keep c.  With a plan, every
+ * lb_spmv(MERGE_PATH) call (L = 504 or 1016) gathers x of the hot and warm columns once (warm
+ * columns ascend, so that gather sweeps x in address order), each CTA stages the hot values in
+ * shared memory, and the tile kernel reads warm values from the dense copy (kept in L2 with an
+ * evict_last policy; cold x reads use evict_first).  Products and summation order are unchanged:
+ * y is bitwise identical to the call without a plan.  Other schedules ignore the plan.
  *  slots          0 = default (16384: 64 KB of shared memory per SM); 1 .. 45056; < 0 drops the plan.
+ *  warm_cols      0 = no warm tier; -1 = auto (a 40 MB budget when x (4*cols bytes) is larger
+ *                 than the L2, else none); > 0 = budget in columns.
  *  hot_cols_out   (optional) number of planned hot columns (0: no plan was kept).
  *  hot_nnz_out    (optional) number of stored entries in hot columns.
- * Cost: device memory 4*nnz + 8*hot + 4*cols (temporary); a degree histogram, 1-4 selection passes
- * and a remap of col_idx; synchronises `stream`.  The caller's arrays are not modified.  Errors:
- * LB_ERR_UNSUPPORTED if col_idx/values are not 32-byte aligned; LB_ERR_OOM.  Re-plan (or drop the
- * plan) after modifying col_idx.
+ * Cost: device memory 4*nnz + 8*(hot + warm) + 4*cols (temporary); a degree histogram, a few
+ * selection passes and a remap of col_idx; synchronises `stream`.  The caller's arrays are not
+ * modified.  Errors: LB_ERR_UNSUPPORTED if col_idx/values are not 32-byte aligned; LB_ERR_OOM;
+ * LB_ERR_INVALID_ARG for slots > 45056 or warm_cols < -1.  Re-plan (or drop the plan) after
+ * modifying col_idx.
  */
-lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, void* stream, int32_t* hot_cols_out, int64_t* hot_nnz_out);
+lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, int64_t warm_cols, void* stream, int32_t* hot_cols_out,
+                              int64_t* hot_nnz_out);
 
-/* lb_csr_hot_plan -- inspect the plan (tests): *hot_n = number of hot columns (0: no plan),
- * *hot_nnz = their stored entries; when a plan exists and the pointers are non-NULL, copies (stream-
- * ordered, device to device) the slot -> column table into d_hot_cols_out int32[hot_n] and the
- * remapped column stream into d_hot_col_idx_out int32[nnz] (caller-owned device buffers). */
-lb_status_t lb_csr_hot_plan(lb_csr_t A, int32_t* hot_n, int64_t* hot_nnz, int32_t* d_hot_cols_out,
-                            int32_t* d_hot_col_idx_out, void* stream);
+/* lb_csr_hot_plan -- inspect the plan (tests): numbers of hot / warm columns and their stored
+ * entries (0: no plan / no warm tier); when a plan exists, copies (stream-ordered, device to device,
+ * each pointer optional) the hot slot -> column table into d_hot_cols_out int32[hot_n], the warm
+ * index -> column table into d_warm_cols_out int32[warm_n] and the remapped column stream into
+ * d_col_out int32[nnz] (caller-owned device buffers). */
+lb_status_t lb_csr_hot_plan(lb_csr_t A, int32_t* hot_n, int64_t* hot_nnz, int64_t* warm_n, int64_t* warm_nnz,
+                            int32_t* d_hot_cols_out, int32_t* d_warm_cols_out, int32_t* d_col_out, void* stream);
 
 /* Flags for lb_spmv_ex. */
 #define LB_SPMV_REPARTITION 1u /* MERGE_PATH: recompute the partition inside this call */

@@ -46,8 +46,8 @@ def lib():
         L.oracle_partition_nz.argtypes = [i64, i64, p, i64, p]
         L.oracle_partition_nz.restype = i64
         L.oracle_shard_bounds.argtypes = [i64, p, ctypes.c_int32, p]
-        L.oracle_hot_columns.argtypes = [i64, i64, p, ctypes.c_int32, p, p, p, p, p]
-        L.oracle_hot_columns.restype = i64
+        L.oracle_x_plan.argtypes = [i64, i64, p, ctypes.c_int32, i64, p, p, p, p, p, p, p, p]
+        L.oracle_x_plan.restype = i64
         L.oracle_num_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -142,16 +142,24 @@ def num_threads() -> int:
     return int(lib().oracle_num_threads())
 
 
-def hot_columns(col_idx, cols: int, slots: int):
-    """Hot-column plan by definition (oracle_hot_columns): (slot -> column int32[n], remapped
-    col_idx int32[nnz], stored entries in hot columns)."""
+def x_plan(col_idx, cols: int, slots: int, warm: int = 0):
+    """x-reuse plan by definition (oracle_x_plan): (hot slot -> column int32[n], warm index -> column
+    int32[m], remapped col_idx int32[nnz], stored entries in hot columns, in warm columns)."""
     col = _np(col_idx, np.int32)
     nnz = col.size
     deg = np.zeros(max(cols, 1), np.int64)
-    slot_of = np.zeros(max(cols, 1), np.int32)
+    tier = np.zeros(max(cols, 1), np.int32)
     slot_cols = np.zeros(max(slots, 1), np.int32)
+    warm_cols = np.zeros(max(cols, 1), np.int32)
     remapped = np.zeros(max(nnz, 1), np.int32)
-    hn = ctypes.c_int64()
-    n = lib().oracle_hot_columns(cols, nnz, _ptr(col), slots, _ptr(deg), _ptr(slot_of), _ptr(slot_cols),
-                                 _ptr(remapped), ctypes.byref(hn))
-    return slot_cols[:n].copy(), remapped[:nnz].copy(), int(hn.value)
+    nw, hn, wn = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+    n = lib().oracle_x_plan(cols, nnz, _ptr(col), slots, warm, _ptr(deg), _ptr(tier), _ptr(slot_cols),
+                            _ptr(warm_cols), _ptr(remapped), ctypes.byref(nw), ctypes.byref(hn), ctypes.byref(wn))
+    return (slot_cols[:n].copy(), warm_cols[:nw.value].copy(), remapped[:nnz].copy(), int(hn.value),
+            int(wn.value))
+
+
+def hot_columns(col_idx, cols: int, slots: int):
+    """Hot tier only: (slot -> column, remapped col_idx, stored entries in hot columns)."""
+    sc, _, rm, hn, _ = x_plan(col_idx, cols, slots, 0)
+    return sc, rm, hn

@@ -199,52 +199,68 @@ void oracle_shard_bounds(int64_t rows, const int32_t *row_offsets, int32_t G, in
 }
 
 /*
- * Hot-column plan by definition (B200 extension of the merge-path tile processor -- DESIGN.md
- * section 6b and include/lb.h lb_csr_plan_hot_x; the paper has no such step: it only fixes that
- * the tile processor gathers x[col] per nonzero, Listing 3).
- *   deg(c)  = number of entries k with col_idx[k] == c;
- *   candidates = columns with deg >= 2;
- *   if fewer than `slots` candidates: all of them are hot, slots in ascending column order;
- *   else the hot set is the first `slots` candidates in the order (deg descending, column
- *   ascending); with tau = the smallest degree in it, slots go first to hot columns with
- *   deg > tau (ascending column), then to hot columns with deg == tau (ascending column).
- *   remapped[k] = ~slot(col_idx[k]) for hot columns, col_idx[k] otherwise.
- * Plain counting and a selection by repeated maximum search (no sort, no histogram): O(slots*cols),
- * for the small matrices the tests use.  Returns the number of hot columns; *hot_nnz = sum of
- * their degrees.  deg and slot_of are caller scratch of `cols` entries.
+ * x-reuse plan by definition (B200 extension of the merge-path tile processor -- DESIGN.md section 6b
+ * and include/lb.h lb_csr_plan_hot_x; the paper has no such step: it only fixes that the tile
+ * processor gathers x[col] per nonzero, Listing 3).
+ *   deg(c)  = number of entries k with col_idx[k] == c;  candidates = columns with deg >= 2;
+ *   HOT: if fewer than `slots` candidates, all of them, slots in ascending column order; else the
+ *   first `slots` candidates in the order (deg descending, column ascending); with tau1 = the
+ *   smallest degree among them, slots go first to hot columns with deg > tau1 (ascending column),
+ *   then to hot columns with deg == tau1 (ascending column).
+ *   WARM (hot tier full and warm > 0): tau2 = the smallest d >= 2 with #{deg >= d} <= slots + warm;
+ *   if tau2 <= tau1, the non-hot columns with deg >= tau2 in ascending column order; else none.
+ *   remapped[k] = ~slot(c) (hot), cols + warm_index(c) (warm), c otherwise (c = col_idx[k]).
+ * Plain counting and selection by repeated maximum search (no sort, no histogram): O(slots*cols +
+ * cols*max_deg), for the small matrices the tests use.  Returns the number of hot columns;
+ * *n_warm, *hot_nnz, *warm_nnz as named.  deg and tier_of are caller scratch of `cols` entries.
  */
-int64_t oracle_hot_columns(int64_t cols, int64_t nnz, const int32_t *col_idx, int32_t slots,
-                           int64_t *deg, int32_t *slot_of, int32_t *slot_cols, int32_t *remapped,
-                           int64_t *hot_nnz)
+int64_t oracle_x_plan(int64_t cols, int64_t nnz, const int32_t *col_idx, int32_t slots, int64_t warm,
+                      int64_t *deg, int32_t *tier_of, int32_t *slot_cols, int32_t *warm_cols,
+                      int32_t *remapped, int64_t *n_warm, int64_t *hot_nnz, int64_t *warm_nnz)
 {
-    for (int64_t c = 0; c < cols; ++c) { deg[c] = 0; slot_of[c] = -1; }
+    for (int64_t c = 0; c < cols; ++c) { deg[c] = 0; tier_of[c] = -1; }
     for (int64_t k = 0; k < nnz; ++k) deg[col_idx[k]] += 1;
-    int64_t ncand = 0;
-    for (int64_t c = 0; c < cols; ++c) ncand += deg[c] >= 2;
+    int64_t ncand = 0, maxdeg = 0;
+    for (int64_t c = 0; c < cols; ++c) { ncand += deg[c] >= 2; if (deg[c] > maxdeg) maxdeg = deg[c]; }
     int64_t n = 0;
-    *hot_nnz = 0;
+    *hot_nnz = 0; *warm_nnz = 0; *n_warm = 0;
     if (ncand < slots) {
         for (int64_t c = 0; c < cols; ++c)
-            if (deg[c] >= 2) { slot_of[c] = (int32_t)n; slot_cols[n++] = (int32_t)c; *hot_nnz += deg[c]; }
+            if (deg[c] >= 2) { tier_of[c] = (int32_t)n; slot_cols[n++] = (int32_t)c; *hot_nnz += deg[c]; }
     } else {
         /* mark the hot set: `slots` times take the unmarked candidate of largest degree (lowest
-         * column on ties); slot_of = -2 marks "chosen" until slots are numbered below */
-        int64_t tau = 0;
+         * column on ties); tier_of = -2 marks "chosen" until slots are numbered below */
+        int64_t tau1 = 0;
         for (int32_t s = 0; s < slots; ++s) {
             int64_t best = -1;
             for (int64_t c = 0; c < cols; ++c)
-                if (deg[c] >= 2 && slot_of[c] == -1 && (best < 0 || deg[c] > deg[best])) best = c;
-            slot_of[best] = -2;
-            tau = deg[best];
+                if (deg[c] >= 2 && tier_of[c] == -1 && (best < 0 || deg[c] > deg[best])) best = c;
+            tier_of[best] = -2;
+            tau1 = deg[best];
         }
         for (int64_t c = 0; c < cols; ++c)
-            if (slot_of[c] == -2 && deg[c] > tau) { slot_of[c] = (int32_t)n; slot_cols[n++] = (int32_t)c; *hot_nnz += deg[c]; }
+            if (tier_of[c] == -2 && deg[c] > tau1) { tier_of[c] = (int32_t)n; slot_cols[n++] = (int32_t)c; *hot_nnz += deg[c]; }
         for (int64_t c = 0; c < cols; ++c)
-            if (slot_of[c] == -2 && deg[c] == tau) { slot_of[c] = (int32_t)n; slot_cols[n++] = (int32_t)c; *hot_nnz += deg[c]; }
+            if (tier_of[c] == -2 && deg[c] == tau1) { tier_of[c] = (int32_t)n; slot_cols[n++] = (int32_t)c; *hot_nnz += deg[c]; }
+        if (warm > 0) {
+            int64_t tau2 = maxdeg + 1;
+            for (int64_t d = 2; d <= maxdeg + 1; ++d) {
+                int64_t cnt = 0;
+                for (int64_t c = 0; c < cols; ++c) cnt += deg[c] >= d;
+                if (cnt <= (int64_t)slots + warm) { tau2 = d; break; }
+            }
+            if (tau2 <= tau1)
+                for (int64_t c = 0; c < cols; ++c)
+                    if (tier_of[c] == -1 && deg[c] >= tau2) {
+                        tier_of[c] = (int32_t)(n + *n_warm);
+                        warm_cols[(*n_warm)++] = (int32_t)c;
+                        *warm_nnz += deg[c];
+                    }
+        }
     }
     for (int64_t k = 0; k < nnz; ++k) {
-        int32_t sl = slot_of[col_idx[k]];
-        remapped[k] = sl >= 0 ? ~sl : col_idx[k];
+        int32_t c = col_idx[k], t = tier_of[c];
+        remapped[k] = t < 0 ? c : (t < n ? ~t : (int32_t)(cols + (t - n)));
     }
     return n;
 }

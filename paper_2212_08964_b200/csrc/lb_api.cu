@@ -262,6 +262,10 @@ struct lb_csr_s {
   int hot_n = 0;               // planned hot columns (0: no plan)
   int hot_n4 = 0;              // ceil(hot_n / 4)
   int64_t hot_nnz = 0;         // stored entries in hot columns
+  int32_t* warm_cols = nullptr; // [warm_n] warm index -> column (ascending)
+  float* x_warm = nullptr;      // [warm_n] x of the warm columns, gathered every call
+  int warm_n = 0;
+  int64_t warm_nnz = 0;
 };
 
 namespace {
@@ -521,10 +525,11 @@ lb_status_t launch_nz_tiles(lb_csr_s* A, const float* x, float* y, stream_t s) {
 constexpr int kHotSlotsDefault = 16384;  // 64 KB of shared memory per SM (best measured on C3)
 constexpr int kHotSlotsMax = 45056;      // 176 KB
 constexpr int kHotDynMax = kHotSlotsMax * 4;
+constexpr int64_t kWarmDefaultBytes = 40ll << 20;  // warm tier budget when x exceeds the L2
 
-template <int W, int R>
+template <int W, int R, int TIER>
 lb_status_t hot_launch_wr(lb_csr_s* A, const float* x, float* y, stream_t s) {
-  auto k = lbk::merge_stream_kernel<W, R, 1, false, unsigned short, true>;
+  auto k = lbk::merge_stream_kernel<W, R, 1, false, unsigned short, TIER>;
   static int conf_dyn[64] = {0};  // dynamic smem size the carve-out was set for, per device
   const int dyn = A->hot_n4 * 16;
   if (conf_dyn[A->device] != dyn) {
@@ -551,6 +556,7 @@ lb_status_t hot_launch_wr(lb_csr_s* A, const float* x, float* y, stream_t s) {
   a.num_tiles = T; a.tiles_per_cta = tpw;
   a.carry_row = A->carry_row; a.carry_val = A->carry_val; a.ticket = A->ticket;
   a.x_hot = A->x_hot; a.hot_n4 = A->hot_n4;
+  a.x_warm = A->x_warm; a.cols = (int)A->cols;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(W * 32);
@@ -569,30 +575,29 @@ lb_status_t hot_launch_wr(lb_csr_s* A, const float* x, float* y, stream_t s) {
 int hot_warps() {
   const char* env = getenv("LB_HOT_W");
   const int w = env ? atoi(env) : 16;
-  return (w == 8 || w == 16 || w == 20) ? w : 16;
+  return w == 8 ? 8 : 16;
 }
 
 bool hot_usable(const lb_csr_s* A) { return A->hot_n > 0 && A->vec32 && (A->L == 1016 || A->L == 504); }
 
+template <int TIER>
+lb_status_t hot_launch_t(lb_csr_s* A, const float* x, float* y, stream_t s) {
+  const bool w8 = hot_warps() == 8;
+  if (A->L == 1016) return w8 ? hot_launch_wr<8, 4, TIER>(A, x, y, s) : hot_launch_wr<16, 4, TIER>(A, x, y, s);
+  return w8 ? hot_launch_wr<8, 2, TIER>(A, x, y, s) : hot_launch_wr<16, 2, TIER>(A, x, y, s);
+}
+
 lb_status_t hot_launch(lb_csr_s* A, const float* x, float* y, stream_t s) {
-  const int w = hot_warps();
-  if (A->L == 1016) {
-    if (w == 8) return hot_launch_wr<8, 4>(A, x, y, s);
-    if (w == 20) return hot_launch_wr<20, 4>(A, x, y, s);
-    return hot_launch_wr<16, 4>(A, x, y, s);
-  }
-  if (w == 8) return hot_launch_wr<8, 2>(A, x, y, s);
-  if (w == 20) return hot_launch_wr<20, 2>(A, x, y, s);
-  return hot_launch_wr<16, 2>(A, x, y, s);
+  return A->warm_n > 0 ? hot_launch_t<2>(A, x, y, s) : hot_launch_t<1>(A, x, y, s);
 }
 
 // partition (T >= 0) and/or the x_hot gather in one launch
 lb_status_t launch_partition_xhot(const lb_csr_s* A, int64_t L, bool partition, const float* x, stream_t s) {
   const int64_t T = partition ? num_tiles(A->rows, A->nnz, L) : -1;
-  const int64_t n = T + 1 + A->hot_n;
+  const int64_t n = T + 1 + A->hot_n + A->warm_n;
   const int grid = (int)std::max<int64_t>(1, (n + kNT - 1) / kNT);
   lbk::partition_xhot_kernel<<<grid, kNT, 0, s>>>((int)A->rows, (int)A->nnz, A->off, L, T, A->coords, A->hot_cols,
-                                                   A->hot_n, x, A->x_hot);
+                                                   A->hot_n, A->warm_cols, A->warm_n, x, A->x_hot, A->x_warm);
   LB_LAUNCHED();
   return LB_OK;
 }
@@ -600,43 +605,27 @@ lb_status_t launch_partition_xhot(const lb_csr_s* A, int64_t L, bool partition, 
 void drop_plan(lb_csr_s* A) {
   if (A->plan_mem) cudaFree(A->plan_mem);
   A->plan_mem = nullptr;
-  A->hcol = A->hot_cols = nullptr;
-  A->x_hot = nullptr;
-  A->hot_n = A->hot_n4 = 0;
-  A->hot_nnz = 0;
+  A->hcol = A->hot_cols = A->warm_cols = nullptr;
+  A->x_hot = A->x_warm = nullptr;
+  A->hot_n = A->hot_n4 = A->warm_n = 0;
+  A->hot_nnz = A->warm_nnz = 0;
 }
 
-// Builds the plan (see lb.h lb_csr_plan_hot_x).  Synchronises `s` a few times (setup call).
-lb_status_t build_plan(lb_csr_s* A, int slots, stream_t s) {
-  drop_plan(A);
+// Degree level of the K-th most referenced column (candidates: deg >= 2), by successive equal-width
+// histograms of deg over the candidate range.  found = false: fewer than K candidates.  Otherwise
+// tau = the level, above = #{deg > tau} (< K), at = #{deg == tau} (above + at >= K).
+struct Level {
+  bool found = false;
+  int64_t tau = 0, above = 0, at = 0;
+};
+
+lb_status_t find_level(lb_csr_s* A, const int* deg, int* bins, int64_t K, stream_t s, Level* out) {
   const int cols = (int)A->cols;
-  const int64_t nnz = A->nnz;
-  const int nblk = (int)((A->cols + lbk::kHotChunk - 1) / lbk::kHotChunk);
-  // temporaries: deg/smap [cols], bins [kDegBins], block offsets [nblk], totals + hot_nnz
-  const size_t tmp_bytes = align256((size_t)cols * 4) + align256(lbk::kDegBins * 4) + align256((size_t)nblk * 8) +
-                           align256(16) + align256(8);
-  char* tmp = nullptr;
-  if (cudaMalloc(&tmp, tmp_bytes) != cudaSuccess) { cudaGetLastError(); return fail(LB_ERR_OOM, "plan temporaries"); }
-  struct Free { char* p; ~Free() { cudaFree(p); } } free_tmp{tmp};
-  int* deg = reinterpret_cast<int*>(tmp);
-  int* bins = reinterpret_cast<int*>(tmp + align256((size_t)cols * 4));
-  int2* blk = reinterpret_cast<int2*>(reinterpret_cast<char*>(bins) + align256(lbk::kDegBins * 4));
-  int* totals = reinterpret_cast<int*>(reinterpret_cast<char*>(blk) + align256((size_t)nblk * 8));
-  unsigned long long* d_hot_nnz = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(totals) + align256(16));
-
-  const int sms = A->dev->sm_count;
-  LB_CUDA(cudaMemsetAsync(deg, 0, (size_t)cols * 4, s));
-  lbk::col_degree_kernel<<<sms * 8, kNT, 0, s>>>(nnz, A->col, deg);
-  LB_LAUNCHED();
-
-  // threshold: the degree tau of the slots-th hottest column (columns with >= 2 entries only), by
-  // successive equal-width histograms over the candidate degree range [lo, hi)
-  int64_t lo = 2, hi = nnz + 1, above = 0;  // above = #columns with deg >= hi
-  int t_hi = 2, t_tie = -1, tie_budget = 0;
+  int64_t lo = 2, hi = A->nnz + 1, above = 0;  // above = #columns with deg >= hi
   std::vector<int> hb(lbk::kDegBins);
-  const int hgrid = std::max(1, std::min(sms * 4, (cols + kNT - 1) / kNT));
-  while (true) {
-    if (hi <= lo) { t_hi = (int)lo; break; }
+  const int hgrid = std::max(1, std::min(A->dev->sm_count * 4, (cols + kNT - 1) / kNT));
+  *out = Level();
+  while (hi > lo) {
     const int64_t w = (hi - lo + lbk::kDegBins - 1) / lbk::kDegBins;
     LB_CUDA(cudaMemsetAsync(bins, 0, lbk::kDegBins * 4, s));
     lbk::degree_hist_kernel<<<hgrid, kNT, 0, s>>>(cols, deg, lo, hi, w, bins);
@@ -647,49 +636,99 @@ lb_status_t build_plan(lb_csr_s* A, int slots, stream_t s) {
     int found = -1;
     for (int b = lbk::kDegBins - 1; b >= 0; --b) {
       if (lo + (int64_t)b * w >= hi) continue;
-      if (cum + hb[b] >= slots) { found = b; break; }
+      if (cum + hb[b] >= K) { found = b; break; }
       cum += hb[b];
     }
-    if (found < 0) { t_hi = (int)lo; break; }  // fewer candidates than slots: all of them
+    if (found < 0) return LB_OK;  // fewer than K candidates
     const int64_t nlo = lo + (int64_t)found * w, nhi = std::min(hi, nlo + w);
     above = cum;
-    if (w == 1) {  // tau = nlo: columns above it all fit; ties fill the remaining slots in column order
-      t_hi = (int)(nlo + 1);
-      t_tie = (int)nlo;
-      tie_budget = (int)(slots - above);
-      break;
+    if (w == 1) {
+      out->found = true;
+      out->tau = nlo;
+      out->above = above;
+      out->at = hb[found];
+      return LB_OK;
     }
     lo = nlo;
     hi = nhi;
   }
+  return LB_OK;
+}
 
-  lbk::hot_count_kernel<<<nblk, 256, 0, s>>>(cols, deg, t_hi, t_tie, blk);
+// Builds the plan (see lb.h lb_csr_plan_hot_x).  Synchronises `s` a few times (setup call).
+lb_status_t build_plan(lb_csr_s* A, int slots, int64_t warm, stream_t s) {
+  drop_plan(A);
+  const int cols = (int)A->cols;
+  const int64_t nnz = A->nnz;
+  const int nblk = (int)((A->cols + lbk::kHotChunk - 1) / lbk::kHotChunk);
+  // temporaries: deg/smap [cols], bins [kDegBins], block offsets [nblk], totals, degree sums
+  const size_t tmp_bytes = align256((size_t)cols * 4) + align256(lbk::kDegBins * 4) + align256((size_t)nblk * 16) +
+                           align256(16) + align256(16);
+  char* tmp = nullptr;
+  if (cudaMalloc(&tmp, tmp_bytes) != cudaSuccess) { cudaGetLastError(); return fail(LB_ERR_OOM, "plan temporaries"); }
+  struct Free { char* p; ~Free() { cudaFree(p); } } free_tmp{tmp};
+  int* deg = reinterpret_cast<int*>(tmp);
+  int* bins = reinterpret_cast<int*>(tmp + align256((size_t)cols * 4));
+  int4* blk = reinterpret_cast<int4*>(reinterpret_cast<char*>(bins) + align256(lbk::kDegBins * 4));
+  int* totals = reinterpret_cast<int*>(reinterpret_cast<char*>(blk) + align256((size_t)nblk * 16));
+  unsigned long long* d_sums = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(totals) + align256(16));
+
+  const int sms = A->dev->sm_count;
+  LB_CUDA(cudaMemsetAsync(deg, 0, (size_t)cols * 4, s));
+  lbk::col_degree_kernel<<<sms * 8, kNT, 0, s>>>(nnz, A->col, deg);
   LB_LAUNCHED();
-  lbk::hot_scan_kernel<<<1, 1024, 0, s>>>(nblk, blk, totals);
+
+  // hot tier: the `slots` most referenced columns (ties at level tau1 in column order)
+  Level l1;
+  lb_status_t st = find_level(A, deg, bins, slots, s, &l1);
+  if (st != LB_OK) return st;
+  int t1_hi = 2, t1_tie = -1, b1 = 0;
+  if (l1.found) { t1_hi = (int)(l1.tau + 1); t1_tie = (int)l1.tau; b1 = (int)(slots - l1.above); }
+  // warm tier: whole degree levels below the hot set, at most `warm` more columns
+  int t2 = INT_MAX, warm_on = 0;
+  if (warm > 0 && l1.found) {
+    Level l2;
+    if ((st = find_level(A, deg, bins, (int64_t)slots + warm, s, &l2)) != LB_OK) return st;
+    const int64_t tau2 = !l2.found ? 2 : (l2.above + l2.at == (int64_t)slots + warm ? l2.tau : l2.tau + 1);
+    if (tau2 <= l1.tau) { t2 = (int)tau2; warm_on = 1; }
+  }
+
+  lbk::plan_count_kernel<<<nblk, 256, 0, s>>>(cols, deg, t1_hi, t1_tie, t2, blk);
   LB_LAUNCHED();
-  int tot[2];
+  lbk::plan_scan_kernel<<<1, 1024, 0, s>>>(nblk, b1, warm_on, blk, totals);
+  LB_LAUNCHED();
+  int tot[4];
   LB_CUDA(cudaMemcpyAsync(tot, totals, sizeof tot, cudaMemcpyDeviceToHost, s));
   LB_CUDA(cudaStreamSynchronize(s));
   const int n_above = tot[0];
-  const int hot_n = n_above + std::min(tie_budget, tot[1]);
+  const int hot_n = n_above + std::min(b1, tot[1]);
+  const int warm_n = warm_on ? tot[3] : 0;
   if (hot_n == 0) return LB_OK;  // nothing worth caching: no plan
 
   const int hot_n4 = (hot_n + 3) / 4;
-  const size_t plan_bytes = align256((size_t)nnz * 4) + align256((size_t)hot_n * 4) + align256((size_t)hot_n4 * 16);
+  const size_t plan_bytes = align256((size_t)nnz * 4) + align256((size_t)hot_n * 4) + align256((size_t)hot_n4 * 16) +
+                            2 * align256((size_t)std::max(warm_n, 1) * 4);
   void* pm = nullptr;
   if (cudaMalloc(&pm, plan_bytes) != cudaSuccess) { cudaGetLastError(); return fail(LB_ERR_OOM, "plan (%zu bytes)", plan_bytes); }
   char* q = static_cast<char*>(pm);
   int32_t* hcol = reinterpret_cast<int32_t*>(q);
-  int32_t* hot_cols = reinterpret_cast<int32_t*>(q + align256((size_t)nnz * 4));
-  float* x_hot = reinterpret_cast<float*>(q + align256((size_t)nnz * 4) + align256((size_t)hot_n * 4));
+  q += align256((size_t)nnz * 4);
+  int32_t* hot_cols = reinterpret_cast<int32_t*>(q);
+  q += align256((size_t)hot_n * 4);
+  float* x_hot = reinterpret_cast<float*>(q);
+  q += align256((size_t)hot_n4 * 16);
+  int32_t* warm_cols = reinterpret_cast<int32_t*>(q);
+  q += align256((size_t)std::max(warm_n, 1) * 4);
+  float* x_warm = reinterpret_cast<float*>(q);
   LB_CUDA(cudaMemsetAsync(x_hot, 0, (size_t)hot_n4 * 16, s));
-  LB_CUDA(cudaMemsetAsync(d_hot_nnz, 0, 8, s));
-  lbk::hot_assign_kernel<<<nblk, 256, 0, s>>>(cols, deg, t_hi, t_tie, n_above, tie_budget, blk, hot_cols, d_hot_nnz);
+  LB_CUDA(cudaMemsetAsync(d_sums, 0, 16, s));
+  lbk::plan_assign_kernel<<<nblk, 256, 0, s>>>(cols, deg, t1_hi, t1_tie, t2, n_above, b1, hot_n, blk, hot_cols,
+                                               warm_cols, d_sums);
   LB_LAUNCHED();
-  lbk::hot_remap_kernel<<<sms * 8, kNT, 0, s>>>(nnz, A->col, deg, hcol);
+  lbk::plan_remap_kernel<<<sms * 8, kNT, 0, s>>>(nnz, cols, hot_n, A->col, deg, hcol);
   LB_LAUNCHED();
-  unsigned long long hn = 0;
-  LB_CUDA(cudaMemcpyAsync(&hn, d_hot_nnz, 8, cudaMemcpyDeviceToHost, s));
+  unsigned long long sums[2] = {0, 0};
+  LB_CUDA(cudaMemcpyAsync(sums, d_sums, sizeof sums, cudaMemcpyDeviceToHost, s));
   LB_CUDA(cudaStreamSynchronize(s));
   A->plan_mem = pm;
   A->hcol = hcol;
@@ -697,7 +736,11 @@ lb_status_t build_plan(lb_csr_s* A, int slots, stream_t s) {
   A->x_hot = x_hot;
   A->hot_n = hot_n;
   A->hot_n4 = hot_n4;
-  A->hot_nnz = (int64_t)hn;
+  A->hot_nnz = (int64_t)sums[0];
+  A->warm_cols = warm_cols;
+  A->x_warm = x_warm;
+  A->warm_n = warm_n;
+  A->warm_nnz = (int64_t)sums[1];
   return LB_OK;
 }
 
@@ -908,7 +951,8 @@ const char* lb_kernel_name(lb_csr_t A, lb_schedule_t sched) {
     case LB_SCHED_MERGE_PATH: {
       if (!A || l_index(A->L) < 0) return "";
       if (hot_usable(A)) {
-        snprintf(buf, sizeof buf, "merge_stream_kernel<%d,%d,1,hot>", hot_warps(), (A->L + 8) / 256);
+        snprintf(buf, sizeof buf, "merge_stream_kernel<%d,%d,1,%s>", hot_warps(), (A->L + 8) / 256,
+                 A->warm_n > 0 ? "hot+warm" : "hot");
         return buf;
       }
       const PipeVariant& v = kVariants[pipe_variant_for(A->L)];
@@ -1021,7 +1065,8 @@ lb_status_t lb_probe_stream_gather(lb_csr_t A, const float* d_x, int32_t reps, v
   return LB_OK;
 }
 
-lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, void* stream, int32_t* hot_cols_out, int64_t* hot_nnz_out) {
+lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, int64_t warm_cols, void* stream, int32_t* hot_cols_out,
+                              int64_t* hot_nnz_out) {
   g_err.clear();
   if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
   if (slots < 0) {
@@ -1029,11 +1074,17 @@ lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, void* stream, int32_t* 
   } else {
     if (slots == 0) slots = kHotSlotsDefault;
     if (slots > kHotSlotsMax) return fail(LB_ERR_INVALID_ARG, "slots %d > %d", slots, kHotSlotsMax);
-    if (!A->vec32) return fail(LB_ERR_UNSUPPORTED, "hot-column plan needs 32-byte aligned col_idx/values");
+    if (warm_cols < -1) return fail(LB_ERR_INVALID_ARG, "warm_cols %lld < -1", (long long)warm_cols);
+    if (!A->vec32) return fail(LB_ERR_UNSUPPORTED, "x-reuse plan needs 32-byte aligned col_idx/values");
+    if (warm_cols == -1) {  // auto: only when x is larger than the L2 (measured: C5 2.2x, C3 -10%)
+      int l2 = 0;
+      LB_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, A->device));
+      warm_cols = 4 * A->cols > (int64_t)l2 ? std::min<int64_t>(A->cols, kWarmDefaultBytes / 4) : 0;
+    }
     if (A->nnz == 0 || A->cols == 0) {
       drop_plan(A);
     } else {
-      lb_status_t st = build_plan(A, slots, S(stream));
+      lb_status_t st = build_plan(A, slots, warm_cols, S(stream));
       if (st != LB_OK) { drop_plan(A); return st; }
     }
   }
@@ -1042,17 +1093,21 @@ lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, void* stream, int32_t* 
   return LB_OK;
 }
 
-lb_status_t lb_csr_hot_plan(lb_csr_t A, int32_t* hot_n, int64_t* hot_nnz, int32_t* d_hot_cols_out,
-                            int32_t* d_hot_col_idx_out, void* stream) {
+lb_status_t lb_csr_hot_plan(lb_csr_t A, int32_t* hot_n, int64_t* hot_nnz, int64_t* warm_n, int64_t* warm_nnz,
+                            int32_t* d_hot_cols_out, int32_t* d_warm_cols_out, int32_t* d_col_out, void* stream) {
   g_err.clear();
   if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
   if (hot_n) *hot_n = A->hot_n;
   if (hot_nnz) *hot_nnz = A->hot_nnz;
+  if (warm_n) *warm_n = A->warm_n;
+  if (warm_nnz) *warm_nnz = A->warm_nnz;
   if (A->hot_n > 0) {
     if (d_hot_cols_out)
       LB_CUDA(cudaMemcpyAsync(d_hot_cols_out, A->hot_cols, (size_t)A->hot_n * 4, cudaMemcpyDeviceToDevice, S(stream)));
-    if (d_hot_col_idx_out)
-      LB_CUDA(cudaMemcpyAsync(d_hot_col_idx_out, A->hcol, (size_t)A->nnz * 4, cudaMemcpyDeviceToDevice, S(stream)));
+    if (d_warm_cols_out && A->warm_n > 0)
+      LB_CUDA(cudaMemcpyAsync(d_warm_cols_out, A->warm_cols, (size_t)A->warm_n * 4, cudaMemcpyDeviceToDevice, S(stream)));
+    if (d_col_out)
+      LB_CUDA(cudaMemcpyAsync(d_col_out, A->hcol, (size_t)A->nnz * 4, cudaMemcpyDeviceToDevice, S(stream)));
   }
   return LB_OK;
 }

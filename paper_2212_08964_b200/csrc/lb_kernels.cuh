@@ -126,11 +126,13 @@ __global__ void partition_kernel(int rows, int nnz, const int* __restrict__ off,
   coords[t] = merge_path_search(rows, nnz, off, t, L);
 }
 
-// The same partition (threads 0..T; T = -1 skips it) fused with the per-call gather of a hot-column
-// plan's x values: threads T+1 .. T+hot_n write x_hot[h] = x[hot_cols[h]] (lb_csr_plan_hot_x).
+// The same partition (threads 0..T; T = -1 skips it) fused with the per-call gathers of an x-reuse
+// plan (lb_csr_plan_hot_x): x_hot[h] = x[hot_cols[h]] (staged in shared memory by the tile kernel)
+// and x_warm[w] = x[warm_cols[w]] (a dense copy of the warm columns that stays in L2).
 __global__ void partition_xhot_kernel(int rows, int nnz, const int* __restrict__ off, int64_t L, int64_t T,
                                       int2* __restrict__ coords, const int* __restrict__ hot_cols, int hot_n,
-                                      const float* __restrict__ x, float* __restrict__ x_hot) {
+                                      const int* __restrict__ warm_cols, int warm_n, const float* __restrict__ x,
+                                      float* __restrict__ x_hot, float* __restrict__ x_warm) {
   asm volatile("griddepcontrol.launch_dependents;");
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t <= T) {
@@ -138,7 +140,12 @@ __global__ void partition_xhot_kernel(int rows, int nnz, const int* __restrict__
     return;
   }
   const int64_t h = t - (T + 1);
-  if (h < hot_n) x_hot[h] = __ldg(x + __ldg(hot_cols + h));
+  if (h < hot_n) {
+    x_hot[h] = __ldg(x + __ldg(hot_cols + h));
+    return;
+  }
+  const int64_t w = h - hot_n;  // warm columns ascend, so these reads sweep x in address order
+  if (w < warm_n) x_warm[w] = __ldg(x + __ldg(warm_cols + w));
 }
 
 // Nonzero-splitting partition (table; reading R19): tiles of L nonzeros, T = max(1,
@@ -430,8 +437,10 @@ struct PipeArgs {
   int* carry_row;
   float* carry_val;
   unsigned* ticket;  // zero before launch; the last CTA resets it
-  const float* x_hot;  // hot-column plan: x of the planned hot columns, gathered this call
+  const float* x_hot;  // x-reuse plan: x of the planned hot columns, gathered this call
   int hot_n4;          // number of float4s of x_hot staged in shared memory (0: no plan)
+  const float* x_warm; // x-reuse plan: x of the warm columns (column stream value cols + w)
+  int cols;
 };
 
 // Tile length for E nonzeros per thread: the 16-byte-aligned nonzero range of a tile spans at
@@ -1072,13 +1081,25 @@ __device__ __forceinline__ void stream_load(const PipeArgs& a, int4 c, int k, in
   }
 }
 
-// One x value.  With a hot-column plan (HOT) the column stream holds ~slot (< 0) for planned hot
-// columns, whose x values sit in shared memory at byte address sxb + 4*slot; other columns are
-// gathered from global x.  One predicated LDS and one predicated LDG, no branch.
-template <bool XKEEP, bool HOT>
-__device__ __forceinline__ float gx(const float* __restrict__ x, uint32_t sxb, int c, uint64_t xpol) {
-  if (HOT) {
-    float v;
+// One x value.  TIER 0: x[c].  With an x-reuse plan the column stream holds ~slot (< 0) for hot
+// columns, whose x values sit in shared memory at byte address sxb + 4*slot (TIER >= 1), and
+// cols + w for warm columns, read from the dense copy x_warm[w] with an L2 evict_last policy while
+// the remaining (cold) columns are read from x with evict_first (TIER 2).  Predicated loads, no
+// branch.
+template <bool XKEEP, int TIER>
+__device__ __forceinline__ float gx(const float* __restrict__ x, const float* __restrict__ xw, int cols, uint32_t sxb,
+                                    int c, uint64_t xpol, uint64_t cpol) {
+  float v;
+  if (TIER == 2) {
+    asm("{\n\t.reg .pred p, q, r;\n\tsetp.lt.s32 p, %1, 0;\n\tsetp.ge.s32 q, %1, %4;\n\tor.pred r, p, q;\n\t"
+        "@p ld.shared.f32 %0, [%2];\n\t"
+        "@q ld.global.nc.L2::cache_hint.f32 %0, [%3], %6;\n\t"
+        "@!r ld.global.nc.L2::cache_hint.f32 %0, [%5], %7;\n\t}"
+        : "=f"(v)
+        : "r"(c), "r"(sxb + ((unsigned)~c << 2)), "l"(xw + (c - cols)), "r"(cols), "l"(x + c), "l"(xpol), "l"(cpol));
+    return v;
+  }
+  if (TIER == 1) {
     asm("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, 0;\n\t@p ld.shared.f32 %0, [%2];\n\t"
         "@!p ld.global.nc.f32 %0, [%3];\n\t}"
         : "=f"(v)
@@ -1090,11 +1111,11 @@ __device__ __forceinline__ float gx(const float* __restrict__ x, uint32_t sxb, i
 
 // the 8 gathers of a lane's round (every loaded column index is valid; positions outside the tile
 // are masked later by zeroing their values)
-template <bool XKEEP, bool HOT>
-__device__ __forceinline__ void gx8(const float* __restrict__ x, uint32_t sxb, const StreamRound& d, float (&xv)[8],
-                                    uint64_t xpol) {
+template <bool XKEEP, int TIER>
+__device__ __forceinline__ void gx8(const float* __restrict__ x, const float* __restrict__ xw, int cols, uint32_t sxb,
+                                    const StreamRound& d, float (&xv)[8], uint64_t xpol, uint64_t cpol) {
 #pragma unroll
-  for (int e = 0; e < 8; ++e) xv[e] = gx<XKEEP, HOT>(x, sxb, d.col[e], xpol);
+  for (int e = 0; e < 8; ++e) xv[e] = gx<XKEEP, TIER>(x, xw, cols, sxb, d.col[e], xpol, cpol);
 }
 
 // y store predicated on `p` (no branch)
@@ -1167,11 +1188,13 @@ __device__ __forceinline__ void tail_clear8(unsigned* p) {
 
 // TailT: unsigned short for merge-path tiles (<= L rows), unsigned for nonzero-split tiles (any
 // number of rows per tile).
-// HOT: the column stream is a hot-column plan's remapped copy (lb_csr_plan_hot_x); the CTA stages
-// the x values of the hot columns (a.x_hot, a.hot_n4 float4s) in dynamic shared memory and serves
-// those gathers from it -- one CTA per SM so the staged copy is shared by all of its warps.
-template <int W, int R, int MINB, bool XKEEP, typename TailT = unsigned short, bool HOT = false>
+// TIER >= 1: the column stream is an x-reuse plan's remapped copy (lb_csr_plan_hot_x); the CTA
+// stages the x values of the hot columns (a.x_hot, a.hot_n4 float4s) in dynamic shared memory and
+// serves those gathers from it -- one CTA per SM so the staged copy is shared by all of its warps.
+// TIER 2 adds the warm columns, read from the dense L2-resident copy a.x_warm.
+template <int W, int R, int MINB, bool XKEEP, typename TailT = unsigned short, int TIER = 0>
 __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) {
+  constexpr bool HOT = TIER >= 1;
   using Cfg = StreamCfg<R>;
   constexpr int K = Cfg::K;
   __shared__ __align__(16) TailT s_tail[W][Cfg::kCap];
@@ -1183,7 +1206,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
   const int t_begin = min(a.num_tiles, gw * a.tiles_per_cta);
   const int t_end = min(a.num_tiles, t_begin + a.tiles_per_cta);
   const uint64_t spol = policy_evict_first();
-  const uint64_t xpol = XKEEP ? policy_evict_last() : 0ull;
+  const uint64_t xpol = (XKEEP || TIER == 2) ? policy_evict_last() : 0ull;
   TailT* tail = s_tail[warp];
   for (int w = lane; w < Cfg::kCap * (int)sizeof(TailT) / 16; w += 32)
     reinterpret_cast<uint4*>(tail)[w] = make_uint4(0u, 0u, 0u, 0u);
@@ -1199,6 +1222,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
   int i_last = t_begin < t_end ? __ldg(&a.coords[t_end].x) : a.rows;
   if (t_begin < t_end) {
     const float* __restrict__ xg = a.x;
+    const float* __restrict__ xw = a.x_warm;
     const uint32_t sxb = HOT ? (uint32_t)__cvta_generic_to_shared(s_xhot) : 0u;
     const int nsteps = (t_end - t_begin) * R;
     // coordinates of tiles t, t+1, t+2 (int4 = i0, j0, i1, j1)
@@ -1216,12 +1240,12 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
     float X0[8], X1[8], X2[8];
     stream_load(a, cT, 0, lane, D0, spol);
     if (1 < nsteps) stream_load(a, R > 1 ? cT : cT1, R > 1 ? 1 : 0, lane, D1, spol);
-    gx8<XKEEP, HOT>(xg, sxb, D0, X0, xpol);
+    gx8<XKEEP, TIER>(xg, xw, a.cols, sxb, D0, X0, xpol, spol);
 
     int t = t_begin, k = 0, st = 0;
     auto step = [&](StreamRound& dc, float (&xc)[8], StreamRound& dn, float (&xn)[8], StreamRound& dl) {
       // (a) gathers for round st+1, loads for round st+2
-      if (st + 1 < nsteps) gx8<XKEEP, HOT>(xg, sxb, dn, xn, xpol);
+      if (st + 1 < nsteps) gx8<XKEEP, TIER>(xg, xw, a.cols, sxb, dn, xn, xpol, spol);
       if (st + 2 < nsteps) {
         const int k2 = k + 2;
         const bool same = k2 < R;
@@ -1391,125 +1415,173 @@ __global__ void __launch_bounds__(256) degree_hist_kernel(int cols, const int* _
     if (h[i]) atomicAdd(bins + i, h[i]);
 }
 
-// Slot assignment in column order.  Column c is hot if deg[c] >= t_hi ("above the threshold"), or
-// deg[c] == t_tie and it is among the first tie_budget such columns.  256 threads x 16 columns per
-// block; hot_count_kernel counts (above, tie) per block, hot_scan_kernel turns the counts into
-// exclusive offsets (one block), hot_assign_kernel writes slots.
+// Tier assignment in column order.  Column c is HOT if deg[c] >= t1_hi, or deg[c] == t1_tie and it
+// is among the first b1 such columns; WARM if it is not hot and deg[c] >= t2.  256 threads x 16
+// columns per block; plan_count_kernel counts (above, tie, >= t2) per block, plan_scan_kernel turns
+// the counts into exclusive offsets (one block), plan_assign_kernel writes the tier map.
 constexpr int kHotPer = 16;
 constexpr int kHotChunk = 256 * kHotPer;
 
-__device__ __forceinline__ int2 block_excl_scan2(int2 v, int2* total) {
-  __shared__ int2 ws[32];
-  __shared__ int2 wtot;
+__device__ __forceinline__ int4 block_excl_scan3(int4 v, int4* total) {
+  __shared__ int4 ws[32];
+  __shared__ int4 wtot;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int a = v.x, b = v.y;
+  int a = v.x, b = v.y, c = v.z;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int ta = __shfl_up_sync(kFull, a, o), tb = __shfl_up_sync(kFull, b, o);
-    if (lane >= o) { a += ta; b += tb; }
+    const int ta = __shfl_up_sync(kFull, a, o), tb = __shfl_up_sync(kFull, b, o), tc = __shfl_up_sync(kFull, c, o);
+    if (lane >= o) { a += ta; b += tb; c += tc; }
   }
-  if (lane == 31) ws[warp] = make_int2(a, b);
+  if (lane == 31) ws[warp] = make_int4(a, b, c, 0);
   __syncthreads();
   if (warp == 0) {
-    int2 w = lane < nw ? ws[lane] : make_int2(0, 0);
-    int wa = w.x, wb = w.y;
+    const int4 w = lane < nw ? ws[lane] : make_int4(0, 0, 0, 0);
+    int wa = w.x, wb = w.y, wc = w.z;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int ta = __shfl_up_sync(kFull, wa, o), tb = __shfl_up_sync(kFull, wb, o);
-      if (lane >= o) { wa += ta; wb += tb; }
+      const int ta = __shfl_up_sync(kFull, wa, o), tb = __shfl_up_sync(kFull, wb, o), tc = __shfl_up_sync(kFull, wc, o);
+      if (lane >= o) { wa += ta; wb += tb; wc += tc; }
     }
-    if (lane < nw) ws[lane] = make_int2(wa - w.x, wb - w.y);  // exclusive warp offsets
-    if (lane == nw - 1) wtot = make_int2(wa, wb);
+    if (lane < nw) ws[lane] = make_int4(wa - w.x, wb - w.y, wc - w.z, 0);  // exclusive warp offsets
+    if (lane == nw - 1) wtot = make_int4(wa, wb, wc, 0);
   }
   __syncthreads();
-  const int2 base = ws[warp];
+  const int4 base = ws[warp];
   if (total) *total = wtot;
-  const int2 r = make_int2(base.x + a - v.x, base.y + b - v.y);
+  const int4 r = make_int4(base.x + a - v.x, base.y + b - v.y, base.z + c - v.z, 0);
   __syncthreads();
   return r;
 }
 
-__global__ void __launch_bounds__(256) hot_count_kernel(int cols, const int* __restrict__ deg, int t_hi, int t_tie,
-                                                        int2* __restrict__ blk) {
+__global__ void __launch_bounds__(256) plan_count_kernel(int cols, const int* __restrict__ deg, int t1_hi, int t1_tie,
+                                                         int t2, int4* __restrict__ blk) {
   const int64_t c0 = (int64_t)blockIdx.x * kHotChunk + (int64_t)threadIdx.x * kHotPer;
-  int a = 0, b = 0;
+  int a = 0, b = 0, c = 0;
 #pragma unroll
   for (int i = 0; i < kHotPer; ++i) {
     if (c0 + i < cols) {
       const int d = __ldg(deg + c0 + i);
-      a += d >= t_hi;
-      b += d == t_tie;
+      a += d >= t1_hi;
+      b += d == t1_tie;
+      c += d >= t2;
     }
   }
-  int2 tot;
-  block_excl_scan2(make_int2(a, b), &tot);
+  int4 tot;
+  block_excl_scan3(make_int4(a, b, c, 0), &tot);
   if (threadIdx.x == 0) blk[blockIdx.x] = tot;
 }
 
-// one block: blk[0..n) counts -> exclusive offsets; totals[0..1] = sums
-__global__ void __launch_bounds__(1024) hot_scan_kernel(int n, int2* __restrict__ blk, int* __restrict__ totals) {
+// one block: per-block counts -> exclusive offsets (x: above t1, y: t1 ties, z: warm); a block's
+// warm count is (>= t2) - above - (ties admitted as hot: clamp(b1 - tie offset, 0, ties)), valid
+// because the host only enables the warm tier (warm_on) with t2 <= t1_tie (every hot column >= t2).
+// totals = (above, ties, >= t2, warm)
+__global__ void __launch_bounds__(1024) plan_scan_kernel(int n, int b1, int warm_on, int4* __restrict__ blk,
+                                                         int* __restrict__ totals) {
   const int per = (n + blockDim.x - 1) / blockDim.x;
   const int b0 = threadIdx.x * per;
-  int a = 0, b = 0;
+  int a = 0, b = 0, c = 0;
   for (int i = 0; i < per; ++i)
-    if (b0 + i < n) { a += blk[b0 + i].x; b += blk[b0 + i].y; }
-  int2 tot;
-  const int2 ex = block_excl_scan2(make_int2(a, b), &tot);
+    if (b0 + i < n) { a += blk[b0 + i].x; b += blk[b0 + i].y; c += blk[b0 + i].z; }
+  int4 tot;
+  const int4 ex = block_excl_scan3(make_int4(a, b, c, 0), &tot);
+  // pass 2 needs each block's tie offset: recompute sequentially per thread, then scan warm counts
   int ra = ex.x, rb = ex.y;
+  int wsum = 0;
   for (int i = 0; i < per; ++i)
     if (b0 + i < n) {
-      const int2 v = blk[b0 + i];
-      blk[b0 + i] = make_int2(ra, rb);
+      const int4 v = blk[b0 + i];
+      const int admitted = min(max(b1 - rb, 0), v.y);
+      wsum += warm_on ? v.z - v.x - admitted : 0;
       ra += v.x;
       rb += v.y;
     }
-  if (threadIdx.x == 0) { totals[0] = tot.x; totals[1] = tot.y; }
+  int4 wtot;
+  const int4 wex = block_excl_scan3(make_int4(wsum, 0, 0, 0), &wtot);
+  ra = ex.x;
+  rb = ex.y;
+  int rw = wex.x;
+  for (int i = 0; i < per; ++i)
+    if (b0 + i < n) {
+      const int4 v = blk[b0 + i];
+      const int admitted = min(max(b1 - rb, 0), v.y);
+      blk[b0 + i] = make_int4(ra, rb, rw, 0);
+      rw += warm_on ? v.z - v.x - admitted : 0;
+      ra += v.x;
+      rb += v.y;
+    }
+  if (threadIdx.x == 0) { totals[0] = tot.x; totals[1] = tot.y; totals[2] = tot.z; totals[3] = wtot.x; }
 }
 
-// deg_smap: in deg[c], out slot of c (-1: not hot); hot_cols[slot] = c; hot_nnz += deg of hot columns
-__global__ void __launch_bounds__(256) hot_assign_kernel(int cols, int* __restrict__ deg_smap, int t_hi, int t_tie,
-                                                         int n_above, int tie_budget, const int2* __restrict__ blk,
-                                                         int* __restrict__ hot_cols,
-                                                         unsigned long long* __restrict__ hot_nnz) {
+// deg_smap: in deg[c]; out -1 (cold), slot s < n_hot (hot), n_hot + w (warm w); hot_cols[s] = c,
+// warm_cols[w] = c; sums[0] += degrees of hot columns, sums[1] += degrees of warm columns
+__global__ void __launch_bounds__(256) plan_assign_kernel(int cols, int* __restrict__ deg_smap, int t1_hi, int t1_tie,
+                                                          int t2, int n_above, int b1, int n_hot,
+                                                          const int4* __restrict__ blk, int* __restrict__ hot_cols,
+                                                          int* __restrict__ warm_cols,
+                                                          unsigned long long* __restrict__ sums) {
   const int64_t c0 = (int64_t)blockIdx.x * kHotChunk + (int64_t)threadIdx.x * kHotPer;
   int d[kHotPer];
   int a = 0, b = 0;
 #pragma unroll
   for (int i = 0; i < kHotPer; ++i) {
     d[i] = c0 + i < cols ? deg_smap[c0 + i] : 0;
-    a += d[i] >= t_hi;
-    b += d[i] == t_tie;
+    a += d[i] >= t1_hi;
+    b += d[i] == t1_tie;
   }
-  const int2 ex = block_excl_scan2(make_int2(a, b), nullptr);
+  // warm count of this thread depends on its tie ranks: computed in the walk below, so the block
+  // scan of warm counts is done on the walk's result
+  const int4 ex = block_excl_scan3(make_int4(a, b, 0, 0), nullptr);
   int ra = blk[blockIdx.x].x + ex.x, rb = blk[blockIdx.x].y + ex.y;
-  unsigned long long sum = 0;
+  int slot[kHotPer];
+  int nw = 0;
+#pragma unroll
+  for (int i = 0; i < kHotPer; ++i) {
+    int sl = -1;
+    if (c0 + i < cols) {
+      if (d[i] >= t1_hi) sl = ra++;
+      else if (d[i] == t1_tie) {
+        if (rb < b1) sl = n_above + rb;
+        ++rb;
+      }
+      if (sl < 0 && d[i] >= t2) { sl = -2; ++nw; }  // warm, numbered below
+    }
+    slot[i] = sl;
+  }
+  const int4 wex = block_excl_scan3(make_int4(nw, 0, 0, 0), nullptr);
+  int rw = blk[blockIdx.x].z + wex.x;
+  unsigned long long hs = 0, wsum = 0;
 #pragma unroll
   for (int i = 0; i < kHotPer; ++i) {
     if (c0 + i >= cols) break;
-    int slot = -1;
-    if (d[i] >= t_hi) slot = ra++;
-    else if (d[i] == t_tie) {
-      if (rb < tie_budget) slot = n_above + rb;
-      ++rb;
+    int v = slot[i];
+    if (v >= 0) {
+      hot_cols[v] = (int)(c0 + i);
+      hs += (unsigned)d[i];
+    } else if (v == -2) {
+      warm_cols[rw] = (int)(c0 + i);
+      wsum += (unsigned)d[i];
+      v = n_hot + rw++;
     }
-    if (slot >= 0) {
-      hot_cols[slot] = (int)(c0 + i);
-      sum += (unsigned)d[i];
-    }
-    deg_smap[c0 + i] = slot;
+    deg_smap[c0 + i] = v;
   }
-  for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
-  if ((threadIdx.x & 31) == 0 && sum) atomicAdd(hot_nnz, sum);
+  for (int o = 16; o > 0; o >>= 1) {
+    hs += __shfl_xor_sync(kFull, hs, o);
+    wsum += __shfl_xor_sync(kFull, wsum, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (hs) atomicAdd(sums, hs);
+    if (wsum) atomicAdd(sums + 1, wsum);
+  }
 }
 
-// hcol[k] = ~slot if col[k] is hot, else col[k]
-__global__ void hot_remap_kernel(int64_t nnz, const int* __restrict__ col, const int* __restrict__ smap,
-                                 int* __restrict__ hcol) {
+// hcol[k] = ~slot (hot), cols + w (warm) or col[k] (cold)
+__global__ void plan_remap_kernel(int64_t nnz, int cols, int n_hot, const int* __restrict__ col,
+                                  const int* __restrict__ smap, int* __restrict__ hcol) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += stride) {
     const int c = __ldcs(col + k);
-    const int sl = __ldg(smap + c);
-    hcol[k] = sl >= 0 ? ~sl : c;
+    const int v = __ldg(smap + c);
+    hcol[k] = v < 0 ? c : (v < n_hot ? ~v : cols + (v - n_hot));
   }
 }
 

@@ -68,8 +68,9 @@ def lib() -> ctypes.CDLL:
         "lb_spmv": ([p, ctypes.c_int, p, p, p], st),
         "lb_spmv_ex": ([p, ctypes.c_int, p, p, u32, p], st),
         "lb_spmm": ([p, i64, p, i64, p, i64, p], st),
-        "lb_csr_plan_hot_x": ([p, i32, p, ctypes.POINTER(i32), ctypes.POINTER(i64)], st),
-        "lb_csr_hot_plan": ([p, ctypes.POINTER(i32), ctypes.POINTER(i64), p, p, p], st),
+        "lb_csr_plan_hot_x": ([p, i32, i64, p, ctypes.POINTER(i32), ctypes.POINTER(i64)], st),
+        "lb_csr_hot_plan": ([p, ctypes.POINTER(i32), ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64),
+                             p, p, p, p], st),
         "lb_spmv_host_workspace_size": ([i64, i64, i64], sz),
         "lb_spmv_host": ([i64, i64, i64, p, p, p, p, p, ctypes.c_int, p, sz, p], st),
         "lb_spmv_phase_times": ([p, ctypes.c_int, p, p, p, ctypes.POINTER(ctypes.c_float)], st),
@@ -249,25 +250,36 @@ class CsrMatrix:
         _check(lib().lb_probe_stream_gather(self.handle, x.data_ptr(), int(reps), _stream(stream), ctypes.byref(ms)))
         return float(ms.value)
 
-    def plan_hot_x(self, slots: int = 0, stream=None) -> tuple[int, int]:
-        """Build (slots >= 0; 0 = library default) or drop (slots < 0) the hot-column plan
-        (lb_csr_plan_hot_x).  Returns (hot columns, stored entries in them)."""
+    def plan_hot_x(self, slots: int = 0, warm: int = -1, stream=None) -> tuple[int, int]:
+        """Build (slots >= 0; 0 = library default) or drop (slots < 0) the x-reuse plan
+        (lb_csr_plan_hot_x; warm: 0 none, -1 auto, > 0 column budget).  Returns (hot columns,
+        stored entries in them); plan_info() has the warm tier."""
         n, h = ctypes.c_int32(), ctypes.c_int64()
-        _check(lib().lb_csr_plan_hot_x(self.handle, int(slots), _stream(stream), ctypes.byref(n), ctypes.byref(h)))
+        _check(lib().lb_csr_plan_hot_x(self.handle, int(slots), int(warm), _stream(stream), ctypes.byref(n),
+                                       ctypes.byref(h)))
         return int(n.value), int(h.value)
 
-    def hot_plan(self, stream=None) -> tuple[torch.Tensor, torch.Tensor] | None:
-        """Copies of the plan's slot->column table and remapped column stream (None without a plan)."""
-        n, h = ctypes.c_int32(), ctypes.c_int64()
-        _check(lib().lb_csr_hot_plan(self.handle, ctypes.byref(n), ctypes.byref(h), None, None, _stream(stream)))
-        if n.value == 0:
+    def plan_info(self) -> dict:
+        n, h, wn, wh = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().lb_csr_hot_plan(self.handle, ctypes.byref(n), ctypes.byref(h), ctypes.byref(wn), ctypes.byref(wh),
+                                     None, None, None, None))
+        return {"hot_cols": int(n.value), "hot_nnz": int(h.value), "warm_cols": int(wn.value),
+                "warm_nnz": int(wh.value)}
+
+    def hot_plan(self, stream=None):
+        """Copies of the plan's hot slot table, warm table and remapped column stream (None without a plan)."""
+        info = self.plan_info()
+        if info["hot_cols"] == 0:
             return None
         dev = self.row_offsets.device
-        hot = torch.empty(n.value, dtype=torch.int32, device=dev)
+        hot = torch.empty(info["hot_cols"], dtype=torch.int32, device=dev)
+        warm = torch.empty(info["warm_cols"], dtype=torch.int32, device=dev)
         hcol = torch.empty(self.nnz, dtype=torch.int32, device=dev)
-        _check(lib().lb_csr_hot_plan(self.handle, ctypes.byref(n), ctypes.byref(h), hot.data_ptr(), hcol.data_ptr(),
+        n, h, wn, wh = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().lb_csr_hot_plan(self.handle, ctypes.byref(n), ctypes.byref(h), ctypes.byref(wn), ctypes.byref(wh),
+                                     hot.data_ptr(), warm.data_ptr() if warm.numel() else None, hcol.data_ptr(),
                                      _stream(stream)))
-        return hot, hcol
+        return hot, warm, hcol
 
     def kernel_name(self, schedule="merge_path") -> str:
         """Main kernel lb_spmv launches for `schedule` (lb_kernel_name)."""

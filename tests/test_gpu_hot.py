@@ -1,8 +1,8 @@
-"""GPU parity of the hot-column plan (lb_csr_plan_hot_x) through the C ABI.
+"""GPU parity of the x-reuse plan (lb_csr_plan_hot_x) through the C ABI.
 
-* the plan (slot table and remapped column stream) is integer work: bit-exact against
-  oracle.hot_columns (small matrices) or against the test-side sort derivation pinned to the oracle
-  in tests/test_oracle_pins.py (full BASELINE.json sizes);
+* the plan (hot slot table, warm table, remapped column stream) is integer work: bit-exact against
+  oracle.x_plan (small matrices) or against the test-side sort derivation pinned to the oracle in
+  tests/test_oracle_pins.py (full BASELINE.json sizes);
 * y with the plan: bit-exact vs the oracle in integer mode, within 1e-5 * s + 1e-30 in float mode,
   and bitwise identical to the merge-path call without a plan (same products, same order).
 """
@@ -14,29 +14,33 @@ import lbgen
 import oracle
 import paper_2212_08964_b200 as lb
 from test_gpu_parity import SMALL, _csr, _packed, _sample_rows, check_y, random_csr, ref
-from test_oracle_pins import hot_columns_by_sort, hot_slot_table_by_sort
+from test_oracle_pins import hot_columns_by_sort, hot_slot_table_by_sort, warm_table_by_levels
 
 pytestmark = pytest.mark.gpu
 
 
-def _plan_matches(M: lb.CsrMatrix, A: lbgen.Csr, slots: int, ref_fn):
-    n, hn = M.plan_hot_x(slots)
-    sc, rm, hn_ref = ref_fn(A.col_idx.cpu().numpy(), A.cols, slots)
+def _plan_matches(M: lb.CsrMatrix, A: lbgen.Csr, slots: int, warm: int, ref_fn):
+    n, hn = M.plan_hot_x(slots, warm)
+    sc, wc, rm, hn_ref, wn_ref = ref_fn(A.col_idx.cpu().numpy(), A.cols, slots, warm)
+    info = M.plan_info()
     assert n == sc.size and hn == hn_ref, (n, sc.size, hn, hn_ref)
+    assert info["warm_cols"] == wc.size and info["warm_nnz"] == wn_ref
     if n:
-        hot, hcol = M.hot_plan()
+        hot, wt, hcol = M.hot_plan()
         assert np.array_equal(hot.cpu().numpy(), sc), "slot table"
+        assert np.array_equal(wt.cpu().numpy(), wc), "warm table"
         assert np.array_equal(hcol.cpu().numpy(), rm), "remapped column stream"
     return n
 
 
+@pytest.mark.parametrize("warm", [0, 1, 100, 5000, 10 ** 7])
 @pytest.mark.parametrize("slots", [1, 5, 333, 4096, 32768, 45056])
 @pytest.mark.parametrize("name", ["rmat12", "rmat14", "skewed", "c1", "stencil100", "uniform_rows"])
-def test_plan_bit_exact(name, slots):
+def test_plan_bit_exact(name, slots, warm):
     A = SMALL[name]("int")
     M = lb.CsrMatrix.from_csr(A)
-    fn = oracle.hot_columns if A.cols * min(slots, A.cols) <= 2e8 else hot_columns_by_sort
-    _plan_matches(M, A, slots, fn)
+    fn = oracle.x_plan if A.cols * min(slots, A.cols) <= 2e8 else hot_columns_by_sort
+    _plan_matches(M, A, slots, warm, fn)
 
 
 @pytest.mark.parametrize("L", [504, 1016])
@@ -50,8 +54,8 @@ def test_spmv_with_plan(name, vmode, L):
     M.set_items_per_tile(L)
     xd = x.cuda()
     y0 = M.spmv(xd, schedule="merge_path", repartition=True).clone()
-    for slots in (7, 2048, 0):
-        n, _ = M.plan_hot_x(slots)
+    for slots, warm in ((7, 0), (2048, 0), (0, 0), (7, 300), (64, 10 ** 6)):
+        n, _ = M.plan_hot_x(slots, warm)
         assert n > 0 or name == "stencil100"
         y = torch.full((A.rows,), float("nan"), device="cuda")
         M.spmv(xd, y, "merge_path", repartition=True)
@@ -64,7 +68,7 @@ def test_spmv_with_plan(name, vmode, L):
         assert torch.equal(y, y0)
 
 
-@pytest.mark.parametrize("W", ["8", "16", "20"])
+@pytest.mark.parametrize("W", ["8", "16"])
 def test_plan_kernel_widths(W, monkeypatch):
     monkeypatch.setenv("LB_HOT_W", W)
     rng = np.random.default_rng(int(W))
@@ -74,7 +78,7 @@ def test_plan_kernel_widths(W, monkeypatch):
         x = lbgen.make_x(A.cols, "int", trial)
         y_ref, s_ref = ref(A, x)
         M = lb.CsrMatrix.from_csr(A)
-        M.plan_hot_x(int(rng.integers(1, 600)))
+        M.plan_hot_x(int(rng.integers(1, 600)), int(rng.integers(0, 3000)))
         for L in (504, 1016):
             M.set_items_per_tile(L)
             check_y(M.spmv(x.cuda(), schedule="merge_path"), y_ref, s_ref, True, f"W{W}/trial{trial}/L{L}")
@@ -84,13 +88,15 @@ def test_plan_edge_cases():
     # x changes between calls: the hot x values are re-gathered every call
     A = lbgen.rmat(12, 16, 3, "int")
     M = lb.CsrMatrix.from_csr(A)
-    assert M.plan_hot_x(1000)[0] == 1000
+    assert M.plan_hot_x(1000, 500)[0] == 1000
+    assert M.plan_info()["warm_cols"] > 0
     for seed in range(3):
         x = lbgen.make_x(A.cols, "int", 100 + seed)
         y_ref, s_ref = ref(A, x)
         check_y(M.spmv(x.cuda(), schedule="merge_path"), y_ref, s_ref, True, f"x seed {seed}")
     # drop the plan
     assert M.plan_hot_x(-1) == (0, 0)
+    assert M.plan_info()["warm_cols"] == 0
     assert M.hot_plan() is None
     assert "hot" not in M.kernel_name("merge_path")
     # no column with two entries: no plan is kept
@@ -118,20 +124,30 @@ def test_plan_full_size(cfg):
     x = lbgen.x_for_config(cfg, A.cols, "float", device="cuda")
     M = lb.CsrMatrix.from_csr(A, device="cuda")
     y0 = M.spmv(x, schedule="merge_path", repartition=True).clone()
-    n, hn = M.plan_hot_x(0)
-    # slot table by the sort derivation (degrees by torch.bincount, test-side), remapped stream
-    # checked on the device by decoding it through the table
+    n, hn = M.plan_hot_x(0, -1)  # library defaults: what bench.py times
+    info = M.plan_info()
+    # tables by the sort derivation (degrees by torch.bincount, test-side), remapped stream checked
+    # on the device by decoding it through the tables
     deg = torch.bincount(A.col_idx.long(), minlength=A.cols).cpu().numpy()
     sc = hot_slot_table_by_sort(deg, 16384)  # library default slot budget
+    warm_budget = (40 << 20) // 4 if 4 * A.cols > torch.cuda.get_device_properties(0).L2_cache_size else 0
+    wc = warm_table_by_levels(deg, sc, 16384, warm_budget)
     assert n == sc.size and hn == int(deg[sc].sum())
-    hot, hcol = M.hot_plan()
+    assert info["warm_cols"] == wc.size and info["warm_nnz"] == int(deg[wc].sum())
+    hot, wt, hcol = M.hot_plan()
     assert np.array_equal(hot.cpu().numpy(), sc)
-    is_hot = torch.zeros(A.cols, dtype=torch.bool, device="cuda")
-    is_hot[hot.long()] = True
-    neg = hcol < 0
-    assert torch.equal(neg, is_hot[A.col_idx.long()])
-    dec = torch.where(neg, hot[(~hcol).clamp(min=0).long()], hcol)
+    assert np.array_equal(wt.cpu().numpy(), wc)
+    table = torch.cat([hot, wt])
+    cold = (hcol >= 0) & (hcol < A.cols)
+    idx = torch.where(hcol < 0, ~hcol, hcol - A.cols + hot.numel()).clamp(min=0, max=max(table.numel() - 1, 0))
+    dec = torch.where(cold, hcol, table[idx.long()])
     assert torch.equal(dec, A.col_idx)
+    tier = torch.full((A.cols,), 2, dtype=torch.int8, device="cuda")
+    tier[wt.long()] = 1
+    tier[hot.long()] = 0
+    got_tier = torch.where(hcol < 0, 0, torch.where(hcol >= A.cols, 1, 2)).to(torch.int8)
+    assert torch.equal(got_tier, tier[A.col_idx.long()])
+    neg = None
     del hcol, dec, neg
     y = torch.full((A.rows,), float("nan"), device="cuda")
     M.spmv(x, y, "merge_path", repartition=True)

@@ -385,15 +385,34 @@ def hot_slot_table_by_sort(deg: np.ndarray, slots: int) -> np.ndarray:
     return np.concatenate([hot[deg[hot] > tau], hot[deg[hot] == tau]]).astype(np.int32)
 
 
-def hot_columns_by_sort(col: np.ndarray, cols: int, slots: int):
-    """Independent derivation of the plan: bincount + lexsort."""
+def warm_table_by_levels(deg: np.ndarray, slot_cols: np.ndarray, slots: int, warm: int) -> np.ndarray:
+    """Warm tier from degrees: whole degree levels via a sorted degree array (the oracle scans levels)."""
+    cand = np.nonzero(deg >= 2)[0]
+    if warm <= 0 or cand.size < slots or slot_cols.size == 0:
+        return np.zeros(0, np.int32)
+    tau1 = deg[slot_cols].min()
+    ds = np.sort(deg[cand])[::-1]  # descending
+    k = slots + warm
+    # smallest d >= 2 with #{deg >= d} <= k: the level just above position k in the sorted list
+    tau2 = 2 if ds.size <= k else int(ds[k]) + 1
+    if tau2 > tau1:
+        return np.zeros(0, np.int32)
+    hot = np.zeros(deg.size, bool)
+    hot[slot_cols] = True
+    return np.nonzero(~hot & (deg >= tau2))[0].astype(np.int32)
+
+
+def hot_columns_by_sort(col: np.ndarray, cols: int, slots: int, warm: int = 0):
+    """Independent derivation of the plan: bincount + lexsort + sorted degree levels."""
     deg = np.bincount(col, minlength=cols).astype(np.int64) if col.size else np.zeros(cols, np.int64)
     slot_cols = hot_slot_table_by_sort(deg, slots)
-    slot_of = np.full(cols, -1, np.int64)
-    slot_of[slot_cols] = np.arange(slot_cols.size)
-    s = slot_of[col] if col.size else np.zeros(0, np.int64)
-    remapped = np.where(s >= 0, ~s, col).astype(np.int32)
-    return slot_cols.astype(np.int32), remapped, int(deg[slot_cols].sum())
+    warm_cols = warm_table_by_levels(deg, slot_cols, slots, warm)
+    tier = np.full(cols, -1, np.int64)
+    tier[slot_cols] = np.arange(slot_cols.size)
+    tier[warm_cols] = slot_cols.size + np.arange(warm_cols.size)
+    t = tier[col] if col.size else np.zeros(0, np.int64)
+    remapped = np.where(t < 0, col, np.where(t < slot_cols.size, ~t, cols + t - slot_cols.size)).astype(np.int32)
+    return slot_cols, warm_cols, remapped, int(deg[slot_cols].sum()), int(deg[warm_cols].sum())
 
 
 def test_hot_columns_worked_examples():
@@ -405,6 +424,15 @@ def test_hot_columns_worked_examples():
         assert hn == case["hot_nnz"], case
         slot_of = {c: i for i, c in enumerate(case["slot_cols"])}
         assert rm.tolist() == [~slot_of[c] if c in slot_of else c for c in g["col_idx"]]
+    w = g["warm"]
+    for case in w["cases"]:
+        sc, wc, rm, hn, wn = oracle.x_plan(w["col_idx"], w["cols"], case["slots"], case["warm"])
+        assert sc.tolist() == case["slot_cols"] and wc.tolist() == case["warm_cols"], case
+        assert (hn, wn) == (case["hot_nnz"], case["warm_nnz"]), case
+        slot_of = {c: i for i, c in enumerate(case["slot_cols"])}
+        warm_of = {c: i for i, c in enumerate(case["warm_cols"])}
+        assert rm.tolist() == [~slot_of[c] if c in slot_of else (w["cols"] + warm_of[c] if c in warm_of else c)
+                               for c in w["col_idx"]], case
 
 
 @pytest.mark.parametrize("seed", range(40))
@@ -416,18 +444,27 @@ def test_hot_columns_match_sort_derivation(seed):
     w = rng.pareto(1.2, cols) + 0.05
     col = rng.choice(cols, size=nnz, p=w / w.sum()).astype(np.int32)
     for slots in (1, 2, 7, int(rng.integers(1, cols + 5)), cols + 10):
-        sc, rm, hn = oracle.hot_columns(col, cols, slots)
-        sc2, rm2, hn2 = hot_columns_by_sort(col, cols, slots)
-        assert np.array_equal(sc, sc2), (seed, slots)
-        assert np.array_equal(rm, rm2), (seed, slots)
-        assert hn == hn2
-        # invariants: every hot column is at least as popular as every non-hot candidate; decoding
-        # the remapped stream through the slot table gives col_idx back
-        deg = np.bincount(col, minlength=cols)
-        hot = np.zeros(cols, bool)
-        hot[sc] = True
-        if (~hot & (deg >= 2)).any() and sc.size:
-            assert deg[sc].min() >= deg[~hot & (deg >= 2)].max()
-        dec = np.where(rm < 0, sc[np.where(rm < 0, ~rm, 0)] if sc.size else 0, rm)
-        assert np.array_equal(dec, col)
-        assert sc.size == min(slots, int((deg >= 2).sum()))
+        for warm in (0, 1, int(rng.integers(1, cols + 5)), 10 * cols):
+            sc, wc, rm, hn, wn = oracle.x_plan(col, cols, slots, warm)
+            sc2, wc2, rm2, hn2, wn2 = hot_columns_by_sort(col, cols, slots, warm)
+            assert np.array_equal(sc, sc2), (seed, slots, warm)
+            assert np.array_equal(wc, wc2), (seed, slots, warm)
+            assert np.array_equal(rm, rm2), (seed, slots, warm)
+            assert (hn, wn) == (hn2, wn2)
+            # invariants: hot columns are at least as popular as warm ones, warm ones at least as
+            # popular as the remaining candidates; the warm tier respects its budget; decoding the
+            # remapped stream through the tables gives col_idx back
+            deg = np.bincount(col, minlength=cols)
+            rest = np.ones(cols, bool)
+            rest[sc] = False
+            rest[wc] = False
+            rest &= deg >= 2
+            if sc.size and wc.size:
+                assert deg[sc].min() >= deg[wc].max()
+            if wc.size and rest.any():
+                assert deg[wc].min() > deg[rest].max()  # whole degree levels
+            assert wc.size <= max(warm, 0)
+            dec = np.where(rm < 0, sc[np.where(rm < 0, ~rm, 0)] if sc.size else 0,
+                           np.where(rm >= cols, wc[np.clip(rm - cols, 0, max(wc.size - 1, 0))] if wc.size else 0, rm))
+            assert np.array_equal(dec, col)
+            assert sc.size == min(slots, int((deg >= 2).sum()))
