@@ -359,7 +359,40 @@ def run_multi(args, cfg):
     stream = torch.cuda.current_stream()
 
     def step():
-        comm.spmv_multi(M, b, x, y, args.schedule)
+        comm.spmv_multi(M, b, x, y, args.schedule, repartition=True)
+
+    def timed(fn, n):
+        dist.barrier()
+        torch.cuda.synchronize()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        for _ in range(n):
+            fn()
+        eb.record(stream)
+        torch.cuda.synchronize()
+        tt = torch.tensor([ea.elapsed_time(eb) / n], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt[0])
+
+    # plain-CSR step rate first, then each rank plans its own shard (x-reuse plan)
+    no_plan, plan = None, None
+    if args.hot_slots >= 0 and args.schedule == "merge_path":
+        for _ in range(3):
+            step()
+        n_np = max(5, min(args.steps, 50))
+        ms_np = timed(step, n_np)
+        no_plan = {"value": round(nnz / (ms_np * 1e-3) / 1e9, 3), "ms_per_step": round(ms_np, 5), "steps": n_np}
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        hot_n, hot_nnz = M.plan_hot_x(args.hot_slots)
+        torch.cuda.synchronize()
+        info = M.plan_info()
+        bt = torch.tensor([(time.perf_counter() - t0) * 1e3], device=dev)
+        dist.all_reduce(bt, op=dist.ReduceOp.MAX)
+        plan = {"kind": "x-reuse plan per shard (lb_csr_plan_hot_x, DESIGN.md 6b)", "slots_requested": args.hot_slots,
+                "rank0_hot_cols": hot_n, "rank0_hot_nnz_frac": round(hot_nnz / max(M.nnz, 1), 4),
+                "rank0_warm_cols": info["warm_cols"], "rank0_warm_nnz_frac": round(info["warm_nnz"] / max(M.nnz, 1), 4),
+                "build_ms_max_over_ranks": round(float(bt[0]), 2), "built": "once per shard, before the timed region"}
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -400,11 +433,11 @@ def run_multi(args, cfg):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (lbgen, seeded)",
             "config": {"workload": cfg, "desc": lbgen.CONFIG_DESC.get(cfg, cfg), "rows": rows, "nnz": nnz,
                        "schedule": args.schedule, "parallelism": f"row shards x{world} (equal nnz), NCCL all-gather of y",
-                       "step": "lb_spmv_multi: shard SpMV + all-gather(v) of y",
+                       "step": "lb_spmv_multi_ex(REPARTITION): shard partition + SpMV + all-gather(v) of y",
                        "l2": "inputs larger than L2; no flush"},
             "plan": plan,
-        "no_plan": no_plan,
-        "gpu_launches": int(launches),
+            "no_plan": no_plan,
+            "gpu_launches": int(launches),
             "spmv_only": {"value": round(nnz / (spmv_ms * 1e-3) / 1e9, 3), "unit": "GNZ/s", "ms": round(spmv_ms, 5)},
             "e2e": None,
         }

@@ -285,6 +285,11 @@ lb_status_t lb_comm_destroy(lb_comm_t c);
 lb_status_t lb_spmv_multi(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, const int64_t* h_bounds,
                           const float* d_x_full, float* d_y_full, void* stream);
 
+/* lb_spmv_multi_ex -- lb_spmv_multi with lb_spmv_ex flags (LB_SPMV_REPARTITION: the rank's merge-path
+ * partition is recomputed inside the call; bench.py's multi-GPU step). */
+lb_status_t lb_spmv_multi_ex(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, const int64_t* h_bounds,
+                             const float* d_x_full, float* d_y_full, uint32_t flags, void* stream);
+
 /* lb_allgather_rows -- the exchange step of lb_spmv_multi alone: rank r contributes
  * d_y_full[b_r .. b_{r+1}) and receives every other rank's slice in place. */
 lb_status_t lb_allgather_rows(lb_comm_t c, const int64_t* h_bounds, float* d_y_full, void* stream);

@@ -1336,6 +1336,11 @@ lb_status_t lb_allgather_rows(lb_comm_t c, const int64_t* h_bounds, float* d_y_f
 
 lb_status_t lb_spmv_multi(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, const int64_t* h_bounds,
                           const float* d_x_full, float* d_y_full, void* stream) {
+  return lb_spmv_multi_ex(A_local, c, sched, h_bounds, d_x_full, d_y_full, 0u, stream);
+}
+
+lb_status_t lb_spmv_multi_ex(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, const int64_t* h_bounds,
+                             const float* d_x_full, float* d_y_full, uint32_t flags, void* stream) {
   g_err.clear();
   if (!A_local || !c || !h_bounds || !d_x_full || !d_y_full) return fail(LB_ERR_INVALID_ARG, "null argument");
   if ((const void*)d_x_full == (const void*)d_y_full) return fail(LB_ERR_INVALID_ARG, "x and y must not alias");
@@ -1343,7 +1348,7 @@ lb_status_t lb_spmv_multi(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, co
   if (b1 - b0 != A_local->rows)
     return fail(LB_ERR_INVALID_ARG, "local shard has %lld rows, bounds say %lld", (long long)A_local->rows,
                 (long long)(b1 - b0));
-  lb_status_t st = spmv_impl(A_local, sched, d_x_full, d_y_full + b0, 0u, S(stream), nullptr);
+  lb_status_t st = spmv_impl(A_local, sched, d_x_full, d_y_full + b0, flags, S(stream), nullptr);
   if (st != LB_OK) return st;
   return lb_allgather_rows(c, h_bounds, d_y_full, stream);
 }

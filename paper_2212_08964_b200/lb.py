@@ -80,6 +80,7 @@ def lib() -> ctypes.CDLL:
         "lb_comm_init": ([p, i32, i32, i32, ctypes.POINTER(p)], st),
         "lb_comm_destroy": ([p], st),
         "lb_spmv_multi": ([p, p, ctypes.c_int, p, p, p, p], st),
+        "lb_spmv_multi_ex": ([p, p, ctypes.c_int, p, p, p, u32, p], st),
         "lb_allgather_rows": ([p, p, p, p], st),
         "lb_kernel_name": ([p, ctypes.c_int], ctypes.c_char_p),
         "lb_select_schedule": ([p, p, ctypes.POINTER(ctypes.c_int)], st),
@@ -388,10 +389,14 @@ class Comm:
             pass
 
     def spmv_multi(self, A_local: CsrMatrix, bounds, x_full: torch.Tensor, y_full: torch.Tensor,
-                   schedule="merge_path", stream=None) -> torch.Tensor:
+                   schedule="merge_path", stream=None, repartition: bool = False) -> torch.Tensor:
         b = np.ascontiguousarray(bounds, dtype=np.int64)
-        _check(lib().lb_spmv_multi(A_local.handle, self._c, _sched(schedule), b.ctypes.data, x_full.data_ptr(),
-                                   y_full.data_ptr(), _stream(stream)))
+        if repartition:
+            _check(lib().lb_spmv_multi_ex(A_local.handle, self._c, _sched(schedule), b.ctypes.data, x_full.data_ptr(),
+                                          y_full.data_ptr(), LB_SPMV_REPARTITION, _stream(stream)))
+        else:
+            _check(lib().lb_spmv_multi(A_local.handle, self._c, _sched(schedule), b.ctypes.data, x_full.data_ptr(),
+                                       y_full.data_ptr(), _stream(stream)))
         return y_full
 
     def allgather_rows(self, bounds, y_full: torch.Tensor, stream=None) -> torch.Tensor:

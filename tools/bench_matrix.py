@@ -29,13 +29,19 @@ for cfg in CFGS:
     M = lb.CsrMatrix.from_csr(A)
     y = torch.empty(A.rows, device="cuda")
     alg = 8 * A.nnz + 4 * (A.rows + 1) + 4 * A.rows + 4 * A.cols
-    for sched in SCHEDS:
+    for sched in SCHEDS + ["merge_path+plan"]:
+        plan = None
+        if sched == "merge_path+plan":
+            sched = "merge_path"
+            M.set_items_per_tile(1016)
+            M.plan_hot_x(0, -1)
+            plan = M.plan_info()
         n = 20 if sched in ("merge_path",) else 5
         if cfg == "c1":
             n = 200
         ms_step = timeit(lambda: M.spmv(x, y, sched, repartition=True), n)
         ms_cached = timeit(lambda: M.spmv(x, y, sched), n)
-        print(json.dumps({"config": cfg, "rows": A.rows, "nnz": A.nnz, "schedule": sched,
+        print(json.dumps({"config": cfg, "rows": A.rows, "nnz": A.nnz, "schedule": sched, "plan": plan,
                           "kernel": M.kernel_name(sched), "L": M.items_per_tile if sched == "merge_path" else None,
                           "ms_step": round(ms_step, 4), "GNZ/s_step": round(A.nnz / ms_step / 1e6, 2),
                           "ms_cached_partition": round(ms_cached, 4),
