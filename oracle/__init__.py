@@ -48,6 +48,8 @@ def lib():
         L.oracle_shard_bounds.argtypes = [i64, p, ctypes.c_int32, p]
         L.oracle_x_plan.argtypes = [i64, i64, p, ctypes.c_int32, i64, p, p, p, p, p, p, p, p]
         L.oracle_x_plan.restype = i64
+        L.oracle_sssp.argtypes = [i64, p, p, p, i64, p, p]
+        L.oracle_sssp.restype = i64
         L.oracle_num_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -163,3 +165,17 @@ def hot_columns(col_idx, cols: int, slots: int):
     """Hot tier only: (slot -> column, remapped col_idx, stored entries in hot columns)."""
     sc, _, rm, hn, _ = x_plan(col_idx, cols, slots, 0)
     return sc, rm, hn
+
+
+def sssp(row_offsets, col_idx, weights, source: int) -> np.ndarray:
+    """Dijkstra distances (fp32, +inf if unreachable) by oracle_sssp; ValueError on a negative weight."""
+    off = _np(row_offsets, np.int32)
+    col = _np(col_idx, np.int32)
+    w = _np(weights, np.float32)
+    n = off.size - 1
+    dist = np.zeros(max(n, 1), np.float32)
+    settled = np.zeros(max(n, 1), np.uint8)
+    r = lib().oracle_sssp(n, _ptr(off), _ptr(col), _ptr(w), int(source), _ptr(dist), _ptr(settled))
+    if r < 0:
+        raise ValueError("negative edge weight")
+    return dist[:n].copy()

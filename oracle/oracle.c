@@ -264,3 +264,36 @@ int64_t oracle_x_plan(int64_t cols, int64_t nnz, const int32_t *col_idx, int32_t
     }
     return n;
 }
+
+/*
+ * Single-source shortest paths by Dijkstra's algorithm (NEXT-4; Listing 5 P:1076-1107 relaxes
+ * dist[neighbor] = min(dist[neighbor], dist[source] + weight) with float distances).
+ * Graph in CSR: row u lists u's out-edges (col_idx = neighbor, values = weight >= 0).  Distances are
+ * fp32 like the paper's `float source_dist`; every tentative distance is the fp32 sum
+ * fl(dist[u] + w), the same monotone edge function the GPU relaxation applies, so both reach the
+ * same least fixed point exactly.  Unreachable vertices get +inf.  Plain O(n^2) selection of the
+ * unsettled vertex with the smallest distance (no heap), for the small graphs the tests use.
+ * Returns -1 if a weight is negative, else the number of settled vertices.
+ */
+int64_t oracle_sssp(int64_t n, const int32_t *row_offsets, const int32_t *col_idx, const float *weights,
+                    int64_t source, float *dist, uint8_t *settled)
+{
+    for (int64_t k = 0; k < row_offsets[n]; ++k)
+        if (!(weights[k] >= 0.0f)) return -1;
+    for (int64_t v = 0; v < n; ++v) { dist[v] = INFINITY; settled[v] = 0; }
+    dist[source] = 0.0f;
+    int64_t done = 0;
+    for (;;) {
+        int64_t u = -1;
+        for (int64_t v = 0; v < n; ++v)
+            if (!settled[v] && dist[v] < INFINITY && (u < 0 || dist[v] < dist[u])) u = v;
+        if (u < 0) break;
+        settled[u] = 1;
+        ++done;
+        for (int64_t k = row_offsets[u]; k < row_offsets[u + 1]; ++k) {
+            float nd = dist[u] + weights[k];   /* fp32 add, as on the GPU */
+            if (nd < dist[col_idx[k]]) dist[col_idx[k]] = nd;
+        }
+    }
+    return done;
+}

@@ -468,3 +468,72 @@ def test_hot_columns_match_sort_derivation(seed):
                            np.where(rm >= cols, wc[np.clip(rm - cols, 0, max(wc.size - 1, 0))] if wc.size else 0, rm))
             assert np.array_equal(dec, col)
             assert sc.size == min(slots, int((deg >= 2).sum()))
+
+
+# ---------------------------------------------------------------- SSSP (NEXT-4, Listing 5)
+
+SSSP_GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "sssp_examples.json")
+
+
+def bellman_ford_f32(off, col, w, n, source):
+    """Independent derivation: synchronous Bellman-Ford rounds over all edges with fp32 adds until no
+    change (the least fixed point of dist[v] = min(dist[v], fl(dist[u] + w)), like Dijkstra's)."""
+    dist = np.full(n, np.inf, np.float32)
+    dist[source] = 0
+    src = np.repeat(np.arange(n), np.diff(off))
+    for _ in range(n + 1):
+        cand = (dist[src] + w.astype(np.float32)).astype(np.float32)
+        new = dist.copy()
+        np.minimum.at(new, col, cand)
+        if np.array_equal(new, dist):
+            return dist
+        dist = new
+    raise AssertionError("no convergence")
+
+
+def test_sssp_worked_examples():
+    for c in json.load(open(SSSP_GOLDEN))["cases"]:
+        got = oracle.sssp(c["off"], c["col"], c["w"], c["source"])
+        want = np.array([np.inf if v == "inf" else v for v in c["dist"]], np.float32)
+        assert np.array_equal(got, want), c["name"]
+
+
+def test_sssp_negative_weight_rejected():
+    with pytest.raises(ValueError):
+        oracle.sssp([0, 1, 1], [1], [-1.0], 0)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_sssp_matches_bellman_ford(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(1, 300))
+    deg = rng.integers(0, 12, n) * (rng.random(n) < 0.8)
+    off = np.zeros(n + 1, np.int64)
+    off[1:] = np.cumsum(deg)
+    col = rng.integers(0, n, int(off[-1])).astype(np.int32)
+    w = (rng.random(int(off[-1])) * rng.choice([1.0, 1e-3, 100.0])).astype(np.float32)
+    w[rng.random(w.size) < 0.05] = 0.0
+    src = int(rng.integers(0, n))
+    got = oracle.sssp(off, col, w, src)
+    assert np.array_equal(got, bellman_ford_f32(off, col, w, n, src))
+
+
+def test_sssp_unit_weights_are_bfs_levels():
+    A = lbgen.rmat(10, 8, 3, "int")
+    off, col = A.row_offsets.numpy(), A.col_idx.numpy()
+    n = A.rows
+    # BFS by frontier sets (closed form: unit weights -> hop counts)
+    level = np.full(n, np.inf, np.float32)
+    level[0] = 0
+    frontier, d = [0], 0
+    while frontier:
+        d += 1
+        nxt = set()
+        for u in frontier:
+            for v in col[off[u]:off[u + 1]]:
+                if level[v] == np.inf:
+                    level[v] = d
+                    nxt.add(int(v))
+        frontier = sorted(nxt)
+    got = oracle.sssp(off, col, np.ones(col.size, np.float32), 0)
+    assert np.array_equal(got, level)
