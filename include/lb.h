@@ -216,6 +216,26 @@ lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, int64_t warm_cols, void
 lb_status_t lb_csr_hot_plan(lb_csr_t A, int32_t* hot_n, int64_t* hot_nnz, int64_t* warm_n, int64_t* warm_nnz,
                             int32_t* d_hot_cols_out, int32_t* d_warm_cols_out, int32_t* d_col_out, void* stream);
 
+/*
+ * lb_sssp -- single-source shortest paths on the graph A (NEXT-4; Listing 5, "Loop until
+ * the frontier is empty"): row u of A lists u's out-edges, col_idx = neighbour, values = weight
+ * (>= 0).  Every round relaxes the out-edges of the current frontier,
+ *   dist[v] = min(dist[v], dist[u] + w)     (fp32 add; atomicMin on the int32 view of non-negative floats)
+ * and the vertices whose distance dropped form the next frontier (each vertex at most once per
+ * round).  The round's edges are load-balanced by `sched`: THREAD_MAPPED (a thread per frontier
+ * vertex), GROUP_MAPPED / BLOCK_MAPPED (a warp takes 32 frontier vertices and strides their pooled
+ * edges, Alg.2), MERGE_PATH / AUTO / NONZERO_SPLIT (frontier vertices + edges split evenly, 16 merge
+ * items per thread, each thread's start found by the 2-D search of Alg.3 over the frontier's
+ * degree prefix).  The result is the least fixed point of the relaxation, identical to Dijkstra
+ * with fp32 path sums (tests/test_gpu_sssp.py).
+ *  source      0 <= source < rows;   d_dist  fp32[rows] device (output; +inf if unreachable).
+ *  rounds_out  (optional) number of frontier rounds.
+ * Requires rows == cols.  Synchronises `stream` once per round.  Allocates a 16*rows-byte workspace
+ * in the handle on first use.  Errors: LB_ERR_INVALID_ARG for a negative or NaN weight (checked
+ * before the first round), a bad source or a non-square matrix.
+ */
+lb_status_t lb_sssp(lb_csr_t A, int64_t source, lb_schedule_t sched, float* d_dist, void* stream, int32_t* rounds_out);
+
 /* Flags for lb_spmv_ex. */
 #define LB_SPMV_REPARTITION 1u /* MERGE_PATH: recompute the partition inside this call */
 

@@ -266,6 +266,14 @@ struct lb_csr_s {
   float* x_warm = nullptr;      // [warm_n] x of the warm columns, gathered every call
   int warm_n = 0;
   int64_t warm_nnz = 0;
+  // SSSP workspace (lb_sssp; allocated on first use)
+  void* sssp_mem = nullptr;
+  int* q_a = nullptr;          // [rows] frontier lists (ping-pong)
+  int* q_b = nullptr;
+  int* stamp = nullptr;        // [rows] round of the last push
+  int* fo = nullptr;           // [rows + 1] frontier degree prefix (merge-path)
+  int* bsum = nullptr;         // [rows / kScanChunk + 2] scan block sums
+  int* counts = nullptr;       // [4] frontier size, next size, negative-weight flag
 };
 
 namespace {
@@ -869,6 +877,83 @@ lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y
   }
 }
 
+// ----------------------------------------------------------------------------- SSSP (NEXT-4)
+lb_status_t sssp_impl(lb_csr_s* A, int64_t source, lb_schedule_t sched, float* dist, stream_t s, int32_t* rounds_out) {
+  if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
+  if (A->rows != A->cols) return fail(LB_ERR_INVALID_ARG, "SSSP needs a square adjacency matrix (rows %lld, cols %lld)",
+                                      (long long)A->rows, (long long)A->cols);
+  if (A->rows == 0) { if (rounds_out) *rounds_out = 0; return LB_OK; }
+  if (source < 0 || source >= A->rows) return fail(LB_ERR_INVALID_ARG, "source %lld out of range", (long long)source);
+  if (!dist) return fail(LB_ERR_INVALID_ARG, "null dist");
+  if (sched == LB_SCHED_AUTO || sched == LB_SCHED_NONZERO_SPLIT) sched = LB_SCHED_MERGE_PATH;
+  if (sched == LB_SCHED_BLOCK_MAPPED) sched = LB_SCHED_GROUP_MAPPED;
+  if (sched != LB_SCHED_MERGE_PATH && sched != LB_SCHED_THREAD_MAPPED && sched != LB_SCHED_GROUP_MAPPED)
+    return fail(LB_ERR_INVALID_ARG, "unknown schedule id %d", (int)sched);
+  const int n = (int)A->rows;
+  const int nb_max = n / lbk::kScanChunk + 2;
+  if (!A->sssp_mem) {
+    const size_t bytes = 3 * align256((size_t)n * 4) + align256(((size_t)n + 1) * 4) + align256((size_t)nb_max * 4 + 4) +
+                         align256(16);
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) { cudaGetLastError(); return fail(LB_ERR_OOM, "SSSP workspace"); }
+    char* q = static_cast<char*>(p);
+    A->sssp_mem = p;
+    A->q_a = reinterpret_cast<int*>(q); q += align256((size_t)n * 4);
+    A->q_b = reinterpret_cast<int*>(q); q += align256((size_t)n * 4);
+    A->stamp = reinterpret_cast<int*>(q); q += align256((size_t)n * 4);
+    A->fo = reinterpret_cast<int*>(q); q += align256(((size_t)n + 1) * 4);
+    A->bsum = reinterpret_cast<int*>(q); q += align256((size_t)nb_max * 4 + 4);
+    A->counts = reinterpret_cast<int*>(q);
+  }
+  const int sms = A->dev->sm_count;
+  lbk::sssp_init_kernel<<<sms * 8, kNT, 0, s>>>(n, (int)source, dist, A->stamp, A->q_a, A->counts);
+  LB_LAUNCHED();
+  if (A->nnz > 0) {
+    lbk::sssp_check_weights_kernel<<<sms * 8, kNT, 0, s>>>(A->nnz, A->val, A->counts + 2);
+    LB_LAUNCHED();
+  }
+  int h[3];
+  LB_CUDA(cudaMemcpyAsync(h, A->counts, sizeof h, cudaMemcpyDeviceToHost, s));
+  LB_CUDA(cudaStreamSynchronize(s));
+  if (h[2]) return fail(LB_ERR_INVALID_ARG, "negative (or NaN) edge weight");
+  int F = 1, round = 0;
+  int* qi = A->q_a;
+  int* qo = A->q_b;
+  while (F > 0) {
+    LB_CUDA(cudaMemsetAsync(A->counts + 1, 0, sizeof(int), s));
+    if (sched == LB_SCHED_THREAD_MAPPED) {
+      lbk::sssp_thread_kernel<<<(F + kNT - 1) / kNT, kNT, 0, s>>>(F, qi, A->off, A->col, A->val, dist, A->stamp, round,
+                                                                   qo, A->counts + 1);
+      LB_LAUNCHED();
+    } else if (sched == LB_SCHED_GROUP_MAPPED) {
+      const int64_t warps = (F + 31) / 32;
+      const int grid = (int)std::min<int64_t>((warps * 32 + kNT - 1) / kNT, (int64_t)sms * 16);
+      lbk::sssp_warp_kernel<<<grid, kNT, 0, s>>>(F, qi, A->off, A->col, A->val, dist, A->stamp, round, qo,
+                                                 A->counts + 1);
+      LB_LAUNCHED();
+    } else {
+      const int nb = (F + lbk::kScanChunk - 1) / lbk::kScanChunk;
+      lbk::frontier_deg_sum_kernel<<<nb, 256, 0, s>>>(F, qi, A->off, A->bsum);
+      LB_LAUNCHED();
+      lbk::frontier_bsum_scan_kernel<<<1, 1024, 0, s>>>(nb, A->bsum);
+      LB_LAUNCHED();
+      lbk::frontier_deg_scan_kernel<<<nb, 256, 0, s>>>(F, qi, A->off, A->bsum, nb, A->fo);
+      LB_LAUNCHED();
+      constexpr int kIpt = 16;  // merge items per thread
+      const int grid = sms * 8;
+      lbk::sssp_merge_kernel<<<grid, kNT, 0, s>>>(F, qi, A->fo, A->off, A->col, A->val, dist, A->stamp, round, qo,
+                                                  A->counts + 1, kIpt);
+      LB_LAUNCHED();
+    }
+    LB_CUDA(cudaMemcpyAsync(&F, A->counts + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LB_CUDA(cudaStreamSynchronize(s));
+    std::swap(qi, qo);
+    ++round;
+  }
+  if (rounds_out) *rounds_out = round;
+  return LB_OK;
+}
+
 constexpr int kSpmmW = 8, kSpmmMinB = 2, kSpmmL = 1016;
 
 template <int P>
@@ -1003,6 +1088,7 @@ lb_status_t lb_csr_destroy(lb_csr_t A) {
   if (!A) return LB_OK;
   if (A->owns_scratch && A->coords) cudaFree(A->coords);
   if (A->plan_mem) cudaFree(A->plan_mem);
+  if (A->sssp_mem) cudaFree(A->sssp_mem);
   delete A;
   return LB_OK;
 }
@@ -1123,6 +1209,11 @@ lb_status_t lb_partition_nz(lb_csr_t A, int32_t items_per_tile, int32_t* d_coord
 lb_status_t lb_spmv(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_y, void* stream) {
   g_err.clear();
   return spmv_impl(A, sched, d_x, d_y, 0u, S(stream), nullptr);
+}
+
+lb_status_t lb_sssp(lb_csr_t A, int64_t source, lb_schedule_t sched, float* d_dist, void* stream, int32_t* rounds_out) {
+  g_err.clear();
+  return sssp_impl(A, source, sched, d_dist, S(stream), rounds_out);
 }
 
 lb_status_t lb_spmm(lb_csr_t A, int64_t n, const float* d_X, int64_t ldx, float* d_Y, int64_t ldy, void* stream) {

@@ -1585,6 +1585,189 @@ __global__ void plan_remap_kernel(int64_t nnz, int cols, int n_hot, const int* _
   }
 }
 
+// ----------------------------------------------------------------------------- SSSP (NEXT-4)
+// Listing 5: each round relaxes the out-edges of the frontier vertices,
+//   dist[v] = atomicMin(dist[v], dist[u] + w(u, v)),  v joins the next frontier if it improved,
+// until the frontier is empty.  Distances are fp32 >= 0 (or +inf), whose bit patterns order like
+// int32, so atomicMin on the int view is the float minimum.  The frontier is a vertex list; a vertex
+// is pushed at most once per round (stamp[v] = round of its last push).  The edges of a round are
+// balanced by the chosen schedule: thread-mapped (a thread per frontier vertex), group-mapped (a warp
+// takes 32 frontier vertices and strides their edge pool, Alg.2) or merge-path (frontier vertices +
+// edges split evenly into per-thread diagonal ranges, each found by the 2-D search, Alg.3).
+
+__device__ __forceinline__ void sssp_relax(int v, float nd, float* __restrict__ dist, int* __restrict__ stamp,
+                                           int round, int* __restrict__ q_out, int* __restrict__ n_out) {
+  const int old = atomicMin(reinterpret_cast<int*>(dist) + v, __float_as_int(nd));
+  if (__float_as_int(nd) < old) {
+    if (atomicExch(stamp + v, round) != round) q_out[atomicAdd(n_out, 1)] = v;
+  }
+}
+
+__global__ void sssp_init_kernel(int n, int source, float* __restrict__ dist, int* __restrict__ stamp,
+                                 int* __restrict__ q_in, int* __restrict__ counts) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+    dist[v] = v == source ? 0.f : __int_as_float(0x7f800000);
+    stamp[v] = -1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    q_in[0] = source;
+    counts[0] = 1;  // frontier size
+    counts[1] = 0;  // next frontier size
+    counts[2] = 0;  // negative-weight flag
+  }
+}
+
+// any weight < 0 (or NaN) sets flag
+__global__ void sssp_check_weights_kernel(int64_t nnz, const float* __restrict__ w, int* flag) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += stride)
+    if (!(__ldg(w + k) >= 0.f)) { atomicExch(flag, 1); return; }
+}
+
+__global__ void sssp_thread_kernel(int F, const int* __restrict__ q_in, const int* __restrict__ off,
+                                   const int* __restrict__ col, const float* __restrict__ w, float* __restrict__ dist,
+                                   int* __restrict__ stamp, int round, int* __restrict__ q_out,
+                                   int* __restrict__ n_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= F) return;
+  const int u = q_in[i];
+  const float du = __ldcg(dist + u);
+  for (int e = __ldg(off + u); e < __ldg(off + u + 1); ++e)
+    sssp_relax(__ldg(col + e), du + __ldg(w + e), dist, stamp, round, q_out, n_out);
+}
+
+// group-mapped (G = 32): a warp takes 32 frontier vertices, scans their degrees and strides the pool
+__global__ void sssp_warp_kernel(int F, const int* __restrict__ q_in, const int* __restrict__ off,
+                                 const int* __restrict__ col, const float* __restrict__ w, float* __restrict__ dist,
+                                 int* __restrict__ stamp, int round, int* __restrict__ q_out, int* __restrict__ n_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t base = gw * 32; base < F; base += nw * 32) {
+    const int64_t i = base + lane;
+    int u = 0, b = 0, cnt = 0;
+    float du = 0.f;
+    if (i < F) {
+      u = q_in[i];
+      b = __ldg(off + u);
+      cnt = __ldg(off + u + 1) - b;
+      du = __ldcg(dist + u);
+    }
+    const int incl = warp_incl_scan_int(cnt, lane);
+    const int total = __shfl_sync(kFull, incl, 31);
+    // uniform trip count so every lane takes part in the shuffles
+    const int rounds_k = (total + 31) / 32;
+    for (int rk = 0; rk < rounds_k; ++rk) {
+      const int k = rk * 32 + lane;
+      int lo = 0;  // first lane whose inclusive prefix exceeds k (binary lifting over the 32 prefixes)
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int cand = lo + step;
+        const int pv = __shfl_sync(kFull, incl, cand - 1);
+        if (pv <= k) lo = cand;
+      }
+      const int src_lane = lo;
+      const int excl = src_lane ? __shfl_sync(kFull, incl, src_lane - 1) : 0;
+      const int bb = __shfl_sync(kFull, b, src_lane);
+      const float dd = __shfl_sync(kFull, du, src_lane);
+      if (k < total) {
+        const int e = bb + (k - excl);
+        sssp_relax(__ldg(col + e), dd + __ldg(w + e), dist, stamp, round, q_out, n_out);
+      }
+    }
+  }
+}
+
+// merge-path over the frontier: items = F frontier "row ends" + E_f edges, fo = exclusive degree
+// prefix of the frontier (fo[F] = E_f); each thread takes `ipt` consecutive merge items found by the
+// 2-D search (Alg.3) and walks them, relaxing the edges it meets (no reduction, no fix-up).
+__global__ void sssp_merge_kernel(int F, const int* __restrict__ q_in, const int* __restrict__ fo,
+                                  const int* __restrict__ off, const int* __restrict__ col,
+                                  const float* __restrict__ w, float* __restrict__ dist, int* __restrict__ stamp,
+                                  int round, int* __restrict__ q_out, int* __restrict__ n_out, int ipt) {
+  const int Ef = __ldcg(fo + F);
+  const int64_t total = (int64_t)F + Ef;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * ipt;
+  for (int64_t d0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * ipt; d0 < total; d0 += stride) {
+    const int64_t d1 = d0 + ipt < total ? d0 + ipt : total;
+    // 2-D search on diagonal d0: i = #{k < F : k + fo[k+1] < d0}
+    int lo = (int)(d0 - Ef > 0 ? d0 - Ef : 0), hi = (int)(d0 < F ? d0 : F);
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if ((int64_t)mid + __ldcg(fo + mid + 1) < d0) lo = mid + 1; else hi = mid;
+    }
+    int i = lo;
+    int j = (int)(d0 - lo);
+    int u = i < F ? q_in[i] : 0;
+    int base = i < F ? __ldg(off + u) - __ldcg(fo + i) : 0;
+    int iend = i < F ? __ldcg(fo + i + 1) : Ef;
+    float du = i < F ? __ldcg(dist + u) : 0.f;
+    for (int64_t d = d0; d < d1; ++d) {
+      if (i < F && j < iend) {  // an edge of frontier vertex i
+        const int e = base + j;
+        sssp_relax(__ldg(col + e), du + __ldg(w + e), dist, stamp, round, q_out, n_out);
+        ++j;
+      } else {  // the end of frontier vertex i
+        ++i;
+        if (i < F) {
+          u = q_in[i];
+          base = __ldg(off + u) - __ldcg(fo + i);
+          iend = __ldcg(fo + i + 1);
+          du = __ldcg(dist + u);
+        }
+      }
+    }
+  }
+}
+
+// exclusive scan of the frontier degrees: fo[i] = sum_{k<i} deg(q_in[k]), fo[F] = total.
+// Three phases: per-block sums (kScanChunk items per block), one-block scan of the block sums, then
+// per-block local scans plus the block offset.
+constexpr int kScanChunk = 2048;  // 256 threads x 8
+__global__ void __launch_bounds__(256) frontier_deg_sum_kernel(int F, const int* __restrict__ q_in,
+                                                               const int* __restrict__ off, int* __restrict__ bsum) {
+  const int b0 = blockIdx.x * kScanChunk + threadIdx.x * 8;
+  int s = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+    if (b0 + e < F) { const int u = q_in[b0 + e]; s += __ldg(off + u + 1) - __ldg(off + u); }
+  int4 tot;
+  block_excl_scan3(make_int4(s, 0, 0, 0), &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot.x;
+}
+__global__ void __launch_bounds__(1024) frontier_bsum_scan_kernel(int nb, int* __restrict__ bsum) {
+  const int per = (nb + blockDim.x - 1) / blockDim.x;
+  const int b0 = threadIdx.x * per;
+  int s = 0;
+  for (int i = 0; i < per; ++i) if (b0 + i < nb) s += bsum[b0 + i];
+  int4 tot;
+  const int4 ex = block_excl_scan3(make_int4(s, 0, 0, 0), &tot);
+  int r = ex.x;
+  for (int i = 0; i < per; ++i)
+    if (b0 + i < nb) { const int v = bsum[b0 + i]; bsum[b0 + i] = r; r += v; }
+  if (threadIdx.x == 0) bsum[nb] = tot.x;
+}
+__global__ void __launch_bounds__(256) frontier_deg_scan_kernel(int F, const int* __restrict__ q_in,
+                                                                const int* __restrict__ off,
+                                                                const int* __restrict__ bsum, int nb,
+                                                                int* __restrict__ fo) {
+  const int b0 = blockIdx.x * kScanChunk + threadIdx.x * 8;
+  int d[8], s = 0;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    d[e] = 0;
+    if (b0 + e < F) { const int u = q_in[b0 + e]; d[e] = __ldg(off + u + 1) - __ldg(off + u); }
+    s += d[e];
+  }
+  const int4 ex = block_excl_scan3(make_int4(s, 0, 0, 0), nullptr);
+  int r = bsum[blockIdx.x] + ex.x;
+#pragma unroll
+  for (int e = 0; e < 8; ++e)
+    if (b0 + e < F) { fo[b0 + e] = r; r += d[e]; }
+  if (blockIdx.x == 0 && threadIdx.x == 0) fo[F] = bsum[nb];
+}
+
 // ----------------------------------------------------------------------------- SpMM (NEXT-2)
 // Y = A X for a panel of P (1 or 4) columns of a row-major X (Listing 4: "a simple loop
 // wrapped around SpMV"), on the same merge-path tiles as SpMV (L = 1016, lb_partition's output is

@@ -71,6 +71,7 @@ def lib() -> ctypes.CDLL:
         "lb_csr_plan_hot_x": ([p, i32, i64, p, ctypes.POINTER(i32), ctypes.POINTER(i64)], st),
         "lb_csr_hot_plan": ([p, ctypes.POINTER(i32), ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64),
                              p, p, p, p], st),
+        "lb_sssp": ([p, i64, ctypes.c_int, p, p, ctypes.POINTER(i32)], st),
         "lb_spmv_host_workspace_size": ([i64, i64, i64], sz),
         "lb_spmv_host": ([i64, i64, i64, p, p, p, p, p, ctypes.c_int, p, sz, p], st),
         "lb_spmv_phase_times": ([p, ctypes.c_int, p, p, p, ctypes.POINTER(ctypes.c_float)], st),
@@ -250,6 +251,17 @@ class CsrMatrix:
         ms = ctypes.c_float()
         _check(lib().lb_probe_stream_gather(self.handle, x.data_ptr(), int(reps), _stream(stream), ctypes.byref(ms)))
         return float(ms.value)
+
+    def sssp(self, source: int, schedule="merge_path", dist: torch.Tensor | None = None,
+             stream=None) -> tuple[torch.Tensor, int]:
+        """Single-source shortest paths over this matrix as a graph (lb_sssp).  Returns (dist, rounds)."""
+        if dist is None:
+            dist = torch.empty(self.rows, dtype=torch.float32, device=self.device)
+        _dev_tensor(dist, torch.float32, "dist", self.rows)
+        r = ctypes.c_int32()
+        _check(lib().lb_sssp(self.handle, int(source), _sched(schedule), dist.data_ptr() if self.rows else None,
+                             _stream(stream), ctypes.byref(r)))
+        return dist, int(r.value)
 
     def plan_hot_x(self, slots: int = 0, warm: int = -1, stream=None) -> tuple[int, int]:
         """Build (slots >= 0; 0 = library default) or drop (slots < 0) the x-reuse plan
