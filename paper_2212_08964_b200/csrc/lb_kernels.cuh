@@ -1668,7 +1668,8 @@ __global__ void sssp_warp_kernel(int F, const int* __restrict__ q_in, const int*
         if (pv <= k) lo = cand;
       }
       const int src_lane = lo;
-      const int excl = src_lane ? __shfl_sync(kFull, incl, src_lane - 1) : 0;
+      const int pe = __shfl_sync(kFull, incl, src_lane > 0 ? src_lane - 1 : 0);  // every lane shuffles
+      const int excl = src_lane ? pe : 0;
       const int bb = __shfl_sync(kFull, b, src_lane);
       const float dd = __shfl_sync(kFull, du, src_lane);
       if (k < total) {
