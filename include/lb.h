@@ -310,6 +310,33 @@ lb_status_t lb_spmv_multi(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, co
 lb_status_t lb_spmv_multi_ex(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, const int64_t* h_bounds,
                              const float* d_x_full, float* d_y_full, uint32_t flags, void* stream);
 
+/*
+ * Fused multi-GPU step (NEXT-1): the all-gather of y is folded into the tile kernel's epilogue.
+ * lb_peer_create registers this rank's y buffer (d_y_full, fp32[rows_global], device; any pointer
+ * inside a cudaMalloc allocation, e.g. a torch tensor) with every rank of `c`: CUDA IPC handles and
+ * offsets are exchanged with NCCL and the other ranks' buffers are mapped into this process
+ * (synchronises `stream`; collective: every rank calls it).  Up to 8 ranks (one NVSwitch node).
+ * lb_spmv_multi_fused then computes this rank's rows of y = A x with the merge-path tile kernel
+ * writing every final y value to its own buffer AND to every peer's buffer over NVLink (rows whose
+ * value the fix-up completes are sent by the fix-up), followed by a cross-rank barrier (an NCCL
+ * group of 4-byte broadcasts), so that in stream order every rank's buffer holds the whole y.  If
+ * no fused kernel applies (schedule other than MERGE_PATH, L other than 504/1016, unaligned
+ * arrays) it computes locally and exchanges with lb_allgather_rows.  x must not alias the buffer.
+ * flags: LB_SPMV_REPARTITION.  lb_peer_destroy unmaps the peers (after all work completed).
+ */
+typedef struct lb_peer_s* lb_peer_t;
+lb_status_t lb_peer_create(lb_comm_t c, float* d_y_full, int64_t rows_global, void* stream, lb_peer_t* out);
+lb_status_t lb_peer_destroy(lb_peer_t p);
+lb_status_t lb_spmv_multi_fused(lb_csr_t A_local, lb_peer_t p, lb_schedule_t sched, const int64_t* h_bounds,
+                                const float* d_x_full, uint32_t flags, void* stream);
+
+/* lb_spmv_peers -- diagnostics for the fused epilogue on one GPU: y = A x (MERGE_PATH) where the tile
+ * kernel also stores every final y value into each of the npeers (<= 7) device buffers h_peer_y[p]
+ * (fp32[rows] each, host array of device pointers) exactly as lb_spmv_multi_fused stores into the
+ * other ranks' buffers.  LB_ERR_UNSUPPORTED if no fused kernel applies to this handle. */
+lb_status_t lb_spmv_peers(lb_csr_t A, const float* d_x, float* d_y, float* const* h_peer_y, int32_t npeers,
+                          uint32_t flags, void* stream);
+
 /* lb_allgather_rows -- the exchange step of lb_spmv_multi alone: rank r contributes
  * d_y_full[b_r .. b_{r+1}) and receives every other rank's slice in place. */
 lb_status_t lb_allgather_rows(lb_comm_t c, const int64_t* h_bounds, float* d_y_full, void* stream);

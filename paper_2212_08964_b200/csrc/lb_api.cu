@@ -535,9 +535,21 @@ constexpr int kHotSlotsMax = 45056;      // 176 KB
 constexpr int kHotDynMax = kHotSlotsMax * 4;
 constexpr int64_t kWarmDefaultBytes = 40ll << 20;  // warm tier budget when x exceeds the L2
 
-template <int W, int R, int TIER>
-lb_status_t hot_launch_wr(lb_csr_s* A, const float* x, float* y, stream_t s) {
-  auto k = lbk::merge_stream_kernel<W, R, 1, false, unsigned short, TIER>;
+// Peer targets of the fused multi-GPU epilogue (lb_spmv_peers / lb_spmv_multi_fused): the other ranks'
+// y, already offset to this rank's first row.
+struct PeerArgs {
+  float* y[lbk::kMaxPeers];
+  int n = 0;
+};
+
+void set_peers(lbk::PipeArgs& a, const PeerArgs* pa) {
+  a.npeers = pa ? pa->n : 0;
+  for (int p = 0; p < lbk::kMaxPeers; ++p) a.peer_y[p] = pa && p < pa->n ? pa->y[p] : nullptr;
+}
+
+template <int W, int R, int TIER, bool PEERS = false>
+lb_status_t hot_launch_wr(lb_csr_s* A, const float* x, float* y, stream_t s, const PeerArgs* pa = nullptr) {
+  auto k = lbk::merge_stream_kernel<W, R, 1, false, unsigned short, TIER, PEERS>;
   static int conf_dyn[64] = {0};  // dynamic smem size the carve-out was set for, per device
   const int dyn = A->hot_n4 * 16;
   if (conf_dyn[A->device] != dyn) {
@@ -565,6 +577,7 @@ lb_status_t hot_launch_wr(lb_csr_s* A, const float* x, float* y, stream_t s) {
   a.carry_row = A->carry_row; a.carry_val = A->carry_val; a.ticket = A->ticket;
   a.x_hot = A->x_hot; a.hot_n4 = A->hot_n4;
   a.x_warm = A->x_warm; a.cols = (int)A->cols;
+  set_peers(a, pa);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(W * 32);
@@ -589,14 +602,54 @@ int hot_warps() {
 bool hot_usable(const lb_csr_s* A) { return A->hot_n > 0 && A->vec32 && (A->L == 1016 || A->L == 504); }
 
 template <int TIER>
-lb_status_t hot_launch_t(lb_csr_s* A, const float* x, float* y, stream_t s) {
+lb_status_t hot_launch_t(lb_csr_s* A, const float* x, float* y, stream_t s, const PeerArgs* pa) {
+  if (pa) {  // fused multi-GPU epilogue: 16 warps per CTA only
+    if (A->L == 1016) return hot_launch_wr<16, 4, TIER, true>(A, x, y, s, pa);
+    return hot_launch_wr<16, 2, TIER, true>(A, x, y, s, pa);
+  }
   const bool w8 = hot_warps() == 8;
   if (A->L == 1016) return w8 ? hot_launch_wr<8, 4, TIER>(A, x, y, s) : hot_launch_wr<16, 4, TIER>(A, x, y, s);
   return w8 ? hot_launch_wr<8, 2, TIER>(A, x, y, s) : hot_launch_wr<16, 2, TIER>(A, x, y, s);
 }
 
-lb_status_t hot_launch(lb_csr_s* A, const float* x, float* y, stream_t s) {
-  return A->warm_n > 0 ? hot_launch_t<2>(A, x, y, s) : hot_launch_t<1>(A, x, y, s);
+lb_status_t hot_launch(lb_csr_s* A, const float* x, float* y, stream_t s, const PeerArgs* pa = nullptr) {
+  return A->warm_n > 0 ? hot_launch_t<2>(A, x, y, s, pa) : hot_launch_t<1>(A, x, y, s, pa);
+}
+
+// Fused epilogue without a plan: the warp-streamed kernel at L = 1016 (8 warps, 2 CTAs per SM, the
+// plain default) or L = 504, with peer stores.
+template <int R>
+lb_status_t peers_stream_launch(lb_csr_s* A, const float* x, float* y, stream_t s, const PeerArgs* pa) {
+  constexpr int W = 8, MINB = 2;
+  auto k = lbk::merge_stream_kernel<W, R, MINB, false, unsigned short, 0, true>;
+  static int blocks_cache[64] = {0};
+  int& blocks = blocks_cache[A->device];
+  if (blocks == 0) {
+    cudaFuncAttributes fa;
+    LB_CUDA(cudaFuncGetAttributes(&fa, k));
+    LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, W * 32, 0));
+    const double need = (double)blocks * (fa.sharedSizeBytes + 1024);
+    const int pct = std::min(100, std::max(1, (int)(100.0 * need / (228.0 * 1024.0)) + 1));
+    LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, W * 32, 0));
+    blocks = std::max(1, blocks);
+  }
+  constexpr int L = 256 * R - 8;
+  const int T = (int)num_tiles(A->rows, A->nnz, L);
+  const int warps_max = std::min(A->dev->sm_count * blocks * W, kMaxCtas);
+  const int tpw = (T + warps_max - 1) / warps_max;
+  const int warps = (T + tpw - 1) / tpw;
+  const int grid = (warps + W - 1) / W;
+  lbk::PipeArgs a;
+  a.off = A->off; a.col = A->col; a.val = A->val; a.x = x; a.y = y;
+  a.coords = A->coords; a.rows = (int)A->rows; a.nnz = (int)A->nnz;
+  a.num_tiles = T; a.tiles_per_cta = tpw;
+  a.carry_row = A->carry_row; a.carry_val = A->carry_val; a.ticket = A->ticket;
+  a.x_hot = nullptr; a.hot_n4 = 0; a.x_warm = nullptr; a.cols = (int)A->cols;
+  set_peers(a, pa);
+  k<<<grid, W * 32, 0, s>>>(a);
+  LB_LAUNCHED();
+  return LB_OK;
 }
 
 // partition (T >= 0) and/or the x_hot gather in one launch
@@ -796,7 +849,8 @@ lb_status_t select_schedule(lb_csr_s* A, stream_t s, lb_schedule_t* out) {
 }
 
 lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y, uint32_t flags, stream_t s,
-                      PhaseEvents* pe) {
+                      PhaseEvents* pe, const PeerArgs* pa = nullptr, bool* fused = nullptr) {
+  if (fused) *fused = false;
   if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
   if (A->rows == 0) return LB_OK;
   if (!y || (!x && A->nnz > 0)) return fail(LB_ERR_INVALID_ARG, "null x or y");
@@ -838,7 +892,20 @@ lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y
         if ((st = launch_partition_xhot(A, A->L, repart, x, s)) != LB_OK) return st;
         if (repart) { A->coords_valid = true; A->coords_L = A->L; A->coords_kind = 0; }
         if (pe) LB_CUDA(cudaEventRecord(pe->ev[1], s));
-        if ((st = hot_launch(A, x, y, s)) != LB_OK) return st;
+        if ((st = hot_launch(A, x, y, s, pa)) != LB_OK) return st;
+        if (fused) *fused = pa != nullptr;
+        if (pe) { LB_CUDA(cudaEventRecord(pe->ev[2], s)); LB_CUDA(cudaEventRecord(pe->ev[3], s)); }
+        return LB_OK;
+      }
+      if (pa && A->vec32 && (A->L == 1016 || A->L == 504)) {  // fused epilogue, plain CSR
+        if (repart) {
+          if ((st = launch_partition(A, A->L, A->coords, s)) != LB_OK) return st;
+          A->coords_valid = true; A->coords_L = A->L; A->coords_kind = 0;
+        }
+        if (pe) LB_CUDA(cudaEventRecord(pe->ev[1], s));
+        st = A->L == 1016 ? peers_stream_launch<4>(A, x, y, s, pa) : peers_stream_launch<2>(A, x, y, s, pa);
+        if (st != LB_OK) return st;
+        if (fused) *fused = true;
         if (pe) { LB_CUDA(cudaEventRecord(pe->ev[2], s)); LB_CUDA(cudaEventRecord(pe->ev[3], s)); }
         return LB_OK;
       }
@@ -1226,6 +1293,25 @@ lb_status_t lb_spmv_ex(lb_csr_t A, lb_schedule_t sched, const float* d_x, float*
   return spmv_impl(A, sched, d_x, d_y, flags, S(stream), nullptr);
 }
 
+lb_status_t lb_spmv_peers(lb_csr_t A, const float* d_x, float* d_y, float* const* h_peer_y, int32_t npeers,
+                          uint32_t flags, void* stream) {
+  g_err.clear();
+  if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
+  if (npeers < 0 || npeers > lbk::kMaxPeers) return fail(LB_ERR_INVALID_ARG, "npeers %d not in [0, %d]", npeers, lbk::kMaxPeers);
+  if (npeers > 0 && !h_peer_y) return fail(LB_ERR_INVALID_ARG, "null peer array");
+  PeerArgs pa;
+  pa.n = npeers;
+  for (int p = 0; p < npeers; ++p) {
+    if (!h_peer_y[p]) return fail(LB_ERR_INVALID_ARG, "null peer %d", p);
+    pa.y[p] = h_peer_y[p];
+  }
+  bool fused = false;
+  lb_status_t st = spmv_impl(A, LB_SCHED_MERGE_PATH, d_x, d_y, flags, S(stream), nullptr, &pa, &fused);
+  if (st != LB_OK) return st;
+  if (!fused) return fail(LB_ERR_UNSUPPORTED, "no fused kernel for this handle (needs L = 504 or 1016 and 32-byte aligned arrays)");
+  return LB_OK;
+}
+
 lb_status_t lb_spmv_phase_times(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_y, void* stream,
                                 float* ms_out) {
   g_err.clear();
@@ -1366,6 +1452,55 @@ struct lb_comm_s {
   int rank = 0, nranks = 1, device = 0;
 };
 
+// A y buffer registered with every rank of a communicator: CUDA IPC handles (plus the offset of the
+// buffer inside its allocation, so PyTorch caching-allocator tensors work) are exchanged over NCCL and
+// the peers' buffers are mapped into this process.
+struct lb_peer_s {
+  lb_comm_s* comm = nullptr;
+  float* y = nullptr;               // this rank's buffer (caller-owned)
+  int64_t rows = 0;
+  float* peer_y[8] = {nullptr};     // index = rank (nullptr for this rank)
+  void* peer_base[8] = {nullptr};   // mapped allocation bases (cudaIpcCloseMemHandle)
+  int* d_flag = nullptr;            // barrier scratch [8]
+  char* d_slots = nullptr;          // exchange buffer (owns d_flag)
+};
+
+namespace {
+
+// allocation base of a device pointer (driver API, loaded at run time)
+lb_status_t alloc_base(const void* p, void** base) {
+  typedef int (*get_range_t)(unsigned long long*, size_t*, unsigned long long);
+  static get_range_t fn = nullptr;
+  if (!fn) {
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libcuda.so.1", RTLD_NOW);
+    if (!h) return fail(LB_ERR_UNSUPPORTED, "cannot load libcuda.so.1");
+    fn = reinterpret_cast<get_range_t>(dlsym(h, "cuMemGetAddressRange_v2"));
+    if (!fn) return fail(LB_ERR_UNSUPPORTED, "cuMemGetAddressRange_v2 missing");
+  }
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (unsigned long long)p) != 0) return fail(LB_ERR_CUDA, "cuMemGetAddressRange failed");
+  *base = reinterpret_cast<void*>(b);
+  return LB_OK;
+}
+
+constexpr int kNcclUint8 = 1;
+
+// every rank ends the call's stream work only after every rank reached it (NCCL group of 4-byte broadcasts)
+lb_status_t peer_barrier(lb_peer_s* p, stream_t s) {
+  lb_comm_s* c = p->comm;
+  LB_NCCL(g_nccl.GroupStart());
+  for (int k = 0; k < c->nranks; ++k) {
+    nccl_result_t r = g_nccl.Broadcast(p->d_flag + k, p->d_flag + k, 4, kNcclUint8, k, c->comm, s);
+    if (r != 0) { g_nccl.GroupEnd(); return fail(LB_ERR_NCCL, "ncclBroadcast: %s", g_nccl.GetErrorString(r)); }
+  }
+  LB_NCCL(g_nccl.GroupEnd());
+  return LB_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 lb_status_t lb_comm_unique_id(uint8_t id_out[128]) {
@@ -1423,6 +1558,94 @@ lb_status_t lb_allgather_rows(lb_comm_t c, const int64_t* h_bounds, float* d_y_f
   LB_NCCL(g_nccl.CommGetAsyncError(c->comm, &ar));
   if (ar != 0) return fail(LB_ERR_NCCL, "NCCL async error: %s", g_nccl.GetErrorString(ar));
   return LB_OK;
+}
+
+lb_status_t lb_peer_create(lb_comm_t c, float* d_y_full, int64_t rows_global, void* stream, lb_peer_t* out) {
+  g_err.clear();
+  if (!c || !d_y_full || !out || rows_global < 0) return fail(LB_ERR_INVALID_ARG, "bad peer-buffer arguments");
+  if (c->nranks > 8) return fail(LB_ERR_UNSUPPORTED, "fused exchange supports up to 8 ranks (one node)");
+  *out = nullptr;
+  stream_t s = S(stream);
+  lb_peer_s* p = new (std::nothrow) lb_peer_s();
+  if (!p) return fail(LB_ERR_OOM, "host allocation failed");
+  p->comm = c;
+  p->y = d_y_full;
+  p->rows = rows_global;
+  struct Slot { cudaIpcMemHandle_t h; int64_t offset; char pad[64 - sizeof(int64_t)]; };
+  static_assert(sizeof(Slot) == 128, "slot size");
+  char* d_slots = nullptr;
+  if (cudaMalloc(&d_slots, sizeof(Slot) * c->nranks + 64) != cudaSuccess) {
+    cudaGetLastError(); delete p; return fail(LB_ERR_OOM, "peer exchange buffer");
+  }
+  p->d_slots = d_slots;
+  p->d_flag = reinterpret_cast<int*>(d_slots + sizeof(Slot) * c->nranks);
+  lb_status_t st = LB_OK;
+  std::vector<Slot> slots(c->nranks);
+  if (c->nranks > 1) {
+    void* base = nullptr;
+    if ((st = alloc_base(d_y_full, &base)) != LB_OK) { cudaFree(d_slots); delete p; return st; }
+    Slot mine = {};
+    if (cudaIpcGetMemHandle(&mine.h, base) != cudaSuccess) {
+      cudaGetLastError(); cudaFree(d_slots); delete p; return fail(LB_ERR_CUDA, "cudaIpcGetMemHandle failed");
+    }
+    mine.offset = reinterpret_cast<char*>(d_y_full) - static_cast<char*>(base);
+    auto run = [&]() -> lb_status_t {
+      LB_CUDA(cudaMemcpyAsync(d_slots + sizeof(Slot) * c->rank, &mine, sizeof(Slot), cudaMemcpyHostToDevice, s));
+      LB_NCCL(g_nccl.GroupStart());
+      for (int k = 0; k < c->nranks; ++k) {
+        char* q = d_slots + sizeof(Slot) * k;
+        nccl_result_t r = g_nccl.Broadcast(q, q, sizeof(Slot), kNcclUint8, k, c->comm, s);
+        if (r != 0) { g_nccl.GroupEnd(); return fail(LB_ERR_NCCL, "ncclBroadcast: %s", g_nccl.GetErrorString(r)); }
+      }
+      LB_NCCL(g_nccl.GroupEnd());
+      LB_CUDA(cudaMemcpyAsync(slots.data(), d_slots, sizeof(Slot) * c->nranks, cudaMemcpyDeviceToHost, s));
+      LB_CUDA(cudaStreamSynchronize(s));
+      for (int k = 0; k < c->nranks; ++k) {
+        if (k == c->rank) continue;
+        void* pb = nullptr;
+        LB_CUDA(cudaIpcOpenMemHandle(&pb, slots[k].h, cudaIpcMemLazyEnablePeerAccess));
+        p->peer_base[k] = pb;
+        p->peer_y[k] = reinterpret_cast<float*>(static_cast<char*>(pb) + slots[k].offset);
+      }
+      return LB_OK;
+    };
+    st = run();
+  }
+  if (st != LB_OK) { lb_peer_destroy(p); return st; }
+  *out = p;
+  return LB_OK;
+}
+
+lb_status_t lb_peer_destroy(lb_peer_t p) {
+  if (!p) return LB_OK;
+  for (int k = 0; k < 8; ++k)
+    if (p->peer_base[k]) cudaIpcCloseMemHandle(p->peer_base[k]);
+  if (p->d_slots) cudaFree(p->d_slots);
+  delete p;
+  return LB_OK;
+}
+
+lb_status_t lb_spmv_multi_fused(lb_csr_t A_local, lb_peer_t peer, lb_schedule_t sched, const int64_t* h_bounds,
+                                const float* d_x_full, uint32_t flags, void* stream) {
+  g_err.clear();
+  if (!A_local || !peer || !h_bounds || !d_x_full) return fail(LB_ERR_INVALID_ARG, "null argument");
+  lb_comm_s* c = peer->comm;
+  if ((const void*)d_x_full == (const void*)peer->y) return fail(LB_ERR_INVALID_ARG, "x and y must not alias");
+  const int64_t b0 = h_bounds[c->rank], b1 = h_bounds[c->rank + 1];
+  if (b1 - b0 != A_local->rows)
+    return fail(LB_ERR_INVALID_ARG, "local shard has %lld rows, bounds say %lld", (long long)A_local->rows,
+                (long long)(b1 - b0));
+  if (h_bounds[c->nranks] != peer->rows) return fail(LB_ERR_INVALID_ARG, "bounds do not match the peer buffer");
+  PeerArgs pa;
+  for (int k = 0; k < c->nranks; ++k)
+    if (k != c->rank) pa.y[pa.n++] = peer->peer_y[k] + b0;
+  bool fused = false;
+  lb_status_t st = spmv_impl(A_local, sched, d_x_full, peer->y + b0, flags, S(stream), nullptr,
+                             pa.n > 0 && sched == LB_SCHED_MERGE_PATH ? &pa : nullptr, &fused);
+  if (st != LB_OK) return st;
+  if (c->nranks == 1) return LB_OK;
+  if (!fused) return lb_allgather_rows(c, h_bounds, peer->y, stream);  // no fused kernel: NCCL exchange
+  return peer_barrier(peer, S(stream));
 }
 
 lb_status_t lb_spmv_multi(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, const int64_t* h_bounds,

@@ -424,6 +424,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+constexpr int kMaxPeers = 7;  // other GPUs of one 8-GPU node
+
 struct PipeArgs {
   const int* off;
   const int* col;
@@ -441,6 +443,8 @@ struct PipeArgs {
   int hot_n4;          // number of float4s of x_hot staged in shared memory (0: no plan)
   const float* x_warm; // x-reuse plan: x of the warm columns (column stream value cols + w)
   int cols;
+  float* peer_y[kMaxPeers];  // fused multi-GPU epilogue: the other ranks' y at this rank's rows
+  int npeers;
 };
 
 // Tile length for E nonzeros per thread: the 16-byte-aligned nonzero range of a tile spans at
@@ -1138,10 +1142,32 @@ __device__ __forceinline__ void stream_prefetch_offsets(const PipeArgs& a, int4 
   }
 }
 
+// y stores of the warp-streamed kernel.  With PEERS the value also goes to every other rank's copy of
+// y (NVLink peer stores: the all-gather of lb_spmv_multi fused into the epilogue);
+// `peers` = false for a partial value (a row the fix-up completes), which stays local.
+template <bool PEERS>
+__device__ __forceinline__ void put_y(const PipeArgs& a, int idx, float v, bool peers = true) {
+  __stcs(a.y + idx, v);
+  if (PEERS && peers) {
+#pragma unroll
+    for (int p = 0; p < kMaxPeers; ++p)
+      if (p < a.npeers) __stcg(a.peer_y[p] + idx, v);
+  }
+}
+template <bool PEERS>
+__device__ __forceinline__ void put_y_if(const PipeArgs& a, float* yt, unsigned rid, int yt_off, float v, bool pred) {
+  st_cs_if(yt + rid, v, pred);
+  if (PEERS) {
+#pragma unroll
+    for (int p = 0; p < kMaxPeers; ++p)
+      if (p < a.npeers && pred) __stcg(a.peer_y[p] + yt_off + (int)rid, v);
+  }
+}
+
 // Row pass of tile c into tail[]: tail[q] = r + 1 when local nonzero q ends row r (r >= 0);
 // rows r > 0 with no nonzero in the tile get y = 0; returns (warp-uniform) whether row 0 has no
 // nonzero in the tile (its value is then the carry entering the tile).
-template <int R, int K, typename TailT>
+template <int R, int K, typename TailT, bool PEERS = false>
 __device__ __forceinline__ bool stream_row_pass(const PipeArgs& a, int4 c, int lane, const int (&lo_)[K],
                                                 const int (&hi_)[K], TailT* tail) {
   const int i0 = c.x, nrows = c.z - c.x, jA = c.y & ~7, lo = c.y - jA;
@@ -1161,7 +1187,7 @@ __device__ __forceinline__ bool stream_row_pass(const PipeArgs& a, int4 c, int l
       const int e = oe - jA;
       const int s = r == 0 ? lo : ob - jA;
       if (e > s) tail[e - 1] = (TailT)(r + 1);
-      else if (r > 0) __stcs(a.y + i0 + r, 0.f);
+      else if (r > 0) put_y<PEERS>(a, i0 + r, 0.f);
       else row0_empty = true;
     }
   }
@@ -1192,7 +1218,7 @@ __device__ __forceinline__ void tail_clear8(unsigned* p) {
 // stages the x values of the hot columns (a.x_hot, a.hot_n4 float4s) in dynamic shared memory and
 // serves those gathers from it -- one CTA per SM so the staged copy is shared by all of its warps.
 // TIER 2 adds the warm columns, read from the dense L2-resident copy a.x_warm.
-template <int W, int R, int MINB, bool XKEEP, typename TailT = unsigned short, int TIER = 0>
+template <int W, int R, int MINB, bool XKEEP, typename TailT = unsigned short, int TIER = 0, bool PEERS = false>
 __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) {
   constexpr bool HOT = TIER >= 1;
   using Cfg = StreamCfg<R>;
@@ -1231,7 +1257,10 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
     int4 cT2 = t_begin + 2 < t_end ? tile_coords(a, t_begin + 2) : cT1;
     int olo[K], ohi[K];
     stream_prefetch_offsets<R, K>(a, cT, lane, olo, ohi);
-    bool r0e = stream_row_pass<R, K, TailT>(a, cT, lane, olo, ohi, tail);
+    // PEERS: the warp's first row is partial when it started before the warp's first tile (the
+    // fix-up completes it and sends it to the peers); every other row this warp writes is final
+    const int open_row = PEERS && cT.x < a.rows && cT.y > __ldg(a.off + cT.x) ? cT.x : -1;
+    bool r0e = stream_row_pass<R, K, TailT, PEERS>(a, cT, lane, olo, ohi, tail);
     if (t_begin + 1 < t_end) stream_prefetch_offsets<R, K>(a, cT1, lane, olo, ohi);
     __syncwarp();
     // three rounds in flight: reduced (gathered), gathering, loading -- rotated by unrolling the
@@ -1254,7 +1283,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
       // (b) the row open at the tile start has no nonzero here: it ends now with the carry
       const int i0 = cT.x;
       if (k == 0 && r0e) {
-        if (lane == 0) __stcs(a.y + i0, rc);
+        if (lane == 0) put_y<PEERS>(a, i0, rc, i0 != open_row);
         rc = 0.f;
       }
       // (c) positions outside the tile's nonzero range [lo, hi) add exactly zero (warp-uniform test)
@@ -1279,7 +1308,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
         run = fmaf(dc.val[e], xc[e], run);
         const unsigned rid = rids[e];
         any |= rid;
-        st_cs_if(yt + rid, run, rid != 0u && first_rid != 0u);
+        put_y_if<PEERS>(a, yt, rid, i0 - 1, run, rid != 0u && first_rid != 0u);
         const bool take = rid != 0u && first_rid == 0u;
         first_val = take ? run : first_val;
         first_rid = take ? rid : first_rid;
@@ -1300,7 +1329,8 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
       if (first_rid != 0u) {
         const bool lf = (B & ((1u << lane) - 1u)) != 0u;  // a row ended in an earlier lane
         const float carry_in = lane == 0 ? rc : (lf ? lval : rc + lval);
-        __stcs(yt + first_rid, carry_in + first_val);
+        const int row = i0 - 1 + (int)first_rid;
+        put_y<PEERS>(a, row, carry_in + first_val, row != open_row);
       }
       if (any) tail_clear8(&tail[256 * k + 8 * lane]);
       rc = B ? agg_v : rc + agg_v;
@@ -1310,7 +1340,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
         ++t;
         __syncwarp();
         if (t < t_end) {
-          r0e = stream_row_pass<R, K, TailT>(a, cT1, lane, olo, ohi, tail);
+          r0e = stream_row_pass<R, K, TailT, PEERS>(a, cT1, lane, olo, ohi, tail);
           if (t + 1 < t_end) stream_prefetch_offsets<R, K>(a, cT2, lane, olo, ohi);
           cT = cT1;
           cT1 = cT2;
@@ -1335,6 +1365,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
     a.carry_row[gw] = i_last;
     a.carry_val[gw] = rc;
   }
+  if (PEERS) __threadfence_system();  // this thread's peer stores are performed before the kernel ends
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
@@ -1351,9 +1382,10 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
       if (c > 0 && __ldcg(a.carry_row + c - 1) == r) continue;
       float sum = 0.f;
       for (int kk = c; kk < nc && __ldcg(a.carry_row + kk) == r; ++kk) sum += __ldcg(a.carry_val + kk);
-      a.y[r] = __ldcg(a.y + r) + sum;
+      put_y<PEERS>(a, r, __ldcg(a.y + r) + sum);
     }
     if (threadIdx.x == 0) *a.ticket = 0u;
+    if (PEERS) __threadfence_system();
   }
 }
 

@@ -83,6 +83,10 @@ def lib() -> ctypes.CDLL:
         "lb_spmv_multi": ([p, p, ctypes.c_int, p, p, p, p], st),
         "lb_spmv_multi_ex": ([p, p, ctypes.c_int, p, p, p, u32, p], st),
         "lb_allgather_rows": ([p, p, p, p], st),
+        "lb_peer_create": ([p, p, i64, p, ctypes.POINTER(p)], st),
+        "lb_peer_destroy": ([p], st),
+        "lb_spmv_multi_fused": ([p, p, ctypes.c_int, p, p, u32, p], st),
+        "lb_spmv_peers": ([p, p, p, p, i32, u32, p], st),
         "lb_kernel_name": ([p, ctypes.c_int], ctypes.c_char_p),
         "lb_select_schedule": ([p, p, ctypes.POINTER(ctypes.c_int)], st),
         "lb_last_error": ([], ctypes.c_char_p),
@@ -263,6 +267,19 @@ class CsrMatrix:
                              _stream(stream), ctypes.byref(r)))
         return dist, int(r.value)
 
+    def spmv_peers(self, x: torch.Tensor, y: torch.Tensor, peers: list, repartition: bool = False,
+                   stream=None) -> torch.Tensor:
+        """lb_spmv_peers: merge-path y = A x whose tile kernel also stores every final y value into each
+        peer tensor (the fused multi-GPU epilogue exercised on one GPU)."""
+        _dev_tensor(x, torch.float32, "x", self.cols)
+        _dev_tensor(y, torch.float32, "y", self.rows)
+        for q in peers:
+            _dev_tensor(q, torch.float32, "peer", self.rows)
+        arr = (ctypes.c_void_p * max(len(peers), 1))(*[q.data_ptr() for q in peers])
+        _check(lib().lb_spmv_peers(self.handle, x.data_ptr(), y.data_ptr(), arr, len(peers),
+                                   LB_SPMV_REPARTITION if repartition else 0, _stream(stream)))
+        return y
+
     def plan_hot_x(self, slots: int = 0, warm: int = -1, stream=None) -> tuple[int, int]:
         """Build (slots >= 0; 0 = library default) or drop (slots < 0) the x-reuse plan
         (lb_csr_plan_hot_x; warm: 0 none, -1 auto, > 0 column budget).  Returns (hot columns,
@@ -411,7 +428,40 @@ class Comm:
                                        y_full.data_ptr(), _stream(stream)))
         return y_full
 
+    def peer_buffer(self, y_full: torch.Tensor, stream=None) -> "PeerBuffer":
+        return PeerBuffer(self, y_full, stream)
+
+    def spmv_multi_fused(self, A_local: CsrMatrix, bounds, x_full: torch.Tensor, peer: "PeerBuffer",
+                         schedule="merge_path", repartition: bool = False, stream=None) -> torch.Tensor:
+        """lb_spmv_multi_fused: shard SpMV whose epilogue writes y into every rank's registered buffer."""
+        b = np.ascontiguousarray(bounds, dtype=np.int64)
+        _check(lib().lb_spmv_multi_fused(A_local.handle, peer._p, _sched(schedule), b.ctypes.data, x_full.data_ptr(),
+                                         LB_SPMV_REPARTITION if repartition else 0, _stream(stream)))
+        return peer.y
+
     def allgather_rows(self, bounds, y_full: torch.Tensor, stream=None) -> torch.Tensor:
         b = np.ascontiguousarray(bounds, dtype=np.int64)
         _check(lib().lb_allgather_rows(self._c, b.ctypes.data, y_full.data_ptr(), _stream(stream)))
         return y_full
+
+
+class PeerBuffer:
+    """A y tensor registered with every rank of a Comm for the fused exchange (lb_peer_create)."""
+
+    def __init__(self, comm: "Comm", y_full: torch.Tensor, stream=None):
+        _dev_tensor(y_full, torch.float32, "y_full")
+        self.y = y_full
+        self.comm = comm
+        self._p = ctypes.c_void_p()
+        _check(lib().lb_peer_create(comm._c, y_full.data_ptr(), y_full.numel(), _stream(stream), ctypes.byref(self._p)))
+
+    def close(self):
+        if self._p:
+            lib().lb_peer_destroy(self._p)
+            self._p = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
