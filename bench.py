@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="budget for the cpu_baseline sample")
     ap.add_argument("--multi", action="store_true", help="use the multi-GPU step even at world size 1 (testing)")
+    ap.add_argument("--fused", action="store_true",
+                    help="multi-GPU step with the all-gather fused into the tile kernel (lb_spmv_multi_fused)")
     ap.add_argument("--hot-slots", type=int, default=0,
                     help="hot-column plan (lb_csr_plan_hot_x) slot budget: 0 = library default, -1 = no plan")
     return ap.parse_args()
@@ -358,8 +360,13 @@ def run_multi(args, cfg):
     y = torch.empty(rows, device=dev)
     stream = torch.cuda.current_stream()
 
+    peer = comm.peer_buffer(y) if args.fused else None
+
     def step():
-        comm.spmv_multi(M, b, x, y, args.schedule, repartition=True)
+        if peer is not None:
+            comm.spmv_multi_fused(M, b, x, peer, args.schedule, repartition=True)
+        else:
+            comm.spmv_multi(M, b, x, y, args.schedule, repartition=True)
 
     def timed(fn, n):
         dist.barrier()
@@ -433,7 +440,9 @@ def run_multi(args, cfg):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (lbgen, seeded)",
             "config": {"workload": cfg, "desc": lbgen.CONFIG_DESC.get(cfg, cfg), "rows": rows, "nnz": nnz,
                        "schedule": args.schedule, "parallelism": f"row shards x{world} (equal nnz), NCCL all-gather of y",
-                       "step": "lb_spmv_multi_ex(REPARTITION): shard partition + SpMV + all-gather(v) of y",
+                       "step": ("lb_spmv_multi_fused(REPARTITION): shard partition + SpMV whose epilogue stores y "
+                                "into every rank's buffer over NVLink + barrier") if args.fused else
+                               "lb_spmv_multi_ex(REPARTITION): shard partition + SpMV + all-gather(v) of y",
                        "l2": "inputs larger than L2; no flush"},
             "plan": plan,
             "no_plan": no_plan,
@@ -444,6 +453,8 @@ def run_multi(args, cfg):
         if sampler:
             rec["clocks"] = sampler.summary()
         print(json.dumps(rec))
+    if peer is not None:
+        peer.close()
     comm.close()
     dist.destroy_process_group()
 
