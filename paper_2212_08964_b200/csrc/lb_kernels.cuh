@@ -25,6 +25,13 @@ namespace lbk {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// Diagnostic ablations of merge_stream_kernel (tools/ablate.sh builds separate libraries with
+// -DLB_ABL=mask; results are WRONG by construction, timings only).  0 in every product build.
+//   1: no y stores in the main loop   2: no segmented scan   4: no row pass / tail reads
+#ifndef LB_ABL
+#define LB_ABL 0
+#endif
+
 // ----------------------------------------------------------------------------- loads
 __device__ __forceinline__ int4 ld_cs_v4(const int* p) { return __ldcs(reinterpret_cast<const int4*>(p)); }
 __device__ __forceinline__ float4 ld_cs_v4(const float* p) { return __ldcs(reinterpret_cast<const float4*>(p)); }
@@ -1172,6 +1179,7 @@ __device__ __forceinline__ bool stream_row_pass(const PipeArgs& a, int4 c, int l
                                                 const int (&hi_)[K], TailT* tail) {
   const int i0 = c.x, nrows = c.z - c.x, jA = c.y & ~7, lo = c.y - jA;
   bool row0_empty = false;
+  if (LB_ABL & 4) return false;
   for (int j = 0; 32 * j < nrows; ++j) {
     const int r = lane + 32 * j;
     if (r < nrows) {
@@ -1299,7 +1307,12 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
       // (d) reduce this round: rows that end inside the lane's 8 nonzeros after its first row end
       // are complete; the first one waits for the carry-in from the lanes before
       unsigned rids[8];
-      tail_read8(&tail[256 * k + 8 * lane], rids);
+      if (LB_ABL & 4) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) rids[e] = (lane == 31 && e == 7) ? 1u : 0u;
+      } else {
+        tail_read8(&tail[256 * k + 8 * lane], rids);
+      }
       float* yt = a.y + i0 - 1;  // row r of the tile ends where rid = r + 1
       unsigned any = 0u, first_rid = 0u;
       float run = 0.f, first_val = 0.f;
@@ -1308,7 +1321,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
         run = fmaf(dc.val[e], xc[e], run);
         const unsigned rid = rids[e];
         any |= rid;
-        put_y_if<PEERS>(a, yt, rid, i0 - 1, run, rid != 0u && first_rid != 0u);
+        if (!(LB_ABL & 1)) put_y_if<PEERS>(a, yt, rid, i0 - 1, run, rid != 0u && first_rid != 0u);
         const bool take = rid != 0u && first_rid == 0u;
         first_val = take ? run : first_val;
         first_rid = take ? rid : first_rid;
@@ -1320,6 +1333,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
       float v = run;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
+        if (LB_ABL & 2) break;
         const float vo = __shfl_up_sync(kFull, v, o);
         const bool reset = lane >= o ? ((B >> (lane - o + 1)) & ((1u << o) - 1u)) != 0u : true;
         if (!reset) v = vo + v;
@@ -1330,9 +1344,9 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
         const bool lf = (B & ((1u << lane) - 1u)) != 0u;  // a row ended in an earlier lane
         const float carry_in = lane == 0 ? rc : (lf ? lval : rc + lval);
         const int row = i0 - 1 + (int)first_rid;
-        put_y<PEERS>(a, row, carry_in + first_val, row != open_row);
+        if (!(LB_ABL & 1) || (LB_ABL & 4)) put_y<PEERS>(a, row, carry_in + first_val, row != open_row);
       }
-      if (any) tail_clear8(&tail[256 * k + 8 * lane]);
+      if (any && !(LB_ABL & 4)) tail_clear8(&tail[256 * k + 8 * lane]);
       rc = B ? agg_v : rc + agg_v;
       // (e) tile t done: row pass of tile t+1 (offsets prefetched), advance coords
       if (++k == R) {
