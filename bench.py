@@ -300,10 +300,12 @@ def run_single(args, cfg):
     try:
         probe_ms = M.probe_stream_gather(x, reps=20)
         rec["roofline_gather"] = {
-            "bound": "l1tex gather (1 L1->L2 request per clock per SM for random 4-byte x[col])",
+            "bound": "l1tex gather (~1 L1TEX line per clock per SM for random 4-byte x[col] not served from shared memory)",
             "achieved": round(nnz / (main_ms * 1e-3) / 1e9, 2), "peak": round(nnz / (probe_ms * 1e-3) / 1e9, 2),
             "unit": "GNZ/s", "frac": round(probe_ms / main_ms, 4),
-            "peak_source": "lb_probe_stream_gather: same col/val/x, 256-bit stream loads + gathers, no rows"}
+            "peak_source": "lb_probe_stream_gather: same col/val/x" + (" and the same x-reuse plan (hot x in shared memory)"
+                                                                     if plan and plan["hot_cols"] else "")
+                           + ", 256-bit stream loads + gathers, no rows"}
     except Exception as e:  # pragma: no cover
         rec["roofline_gather"] = {"error": str(e)}
     if plan is not None and no_plan is not None and ms < no_plan["ms_per_step"]:

@@ -269,7 +269,10 @@ lb_status_t lb_spmv_phase_times(lb_csr_t A, lb_schedule_t sched, const float* d_
  * streams A's col_idx/values with the tile processor's 256-bit loads and gathers x[col] with no
  * row structure, `reps` times; ms_out = mean milliseconds per pass.  nnz / ms_out is the
  * stream+gather ceiling for this matrix on this GPU (the bound of the merge-path tile processor
- * on random-column matrices).  Needs 32-byte aligned col_idx/values.
+ * on random-column matrices).  With an x-reuse plan (lb_csr_plan_hot_x) the
+ * probe streams the plan's column stream and serves hot / warm columns exactly as the tile kernel
+ * does (x_hot staged in shared memory, one CTA of 16 warps per SM) -- the ceiling of the plan.
+ * Needs 32-byte aligned col_idx/values.
  */
 lb_status_t lb_probe_stream_gather(lb_csr_t A, const float* d_x, int32_t reps, void* stream, float* ms_out);
 

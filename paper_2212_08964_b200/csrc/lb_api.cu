@@ -529,7 +529,7 @@ lb_status_t launch_nz_tiles(lb_csr_s* A, const float* x, float* y, stream_t s) {
 // ----------------------------------------------------------------------------- hot-column plan
 // Tile kernel with the plan: warp-streamed, one CTA of W warps per SM, x of the hot columns staged
 // in dynamic shared memory.  W and the slot budget were chosen by measurement;
-// LB_HOT_W overrides W (8, 16, 20) for sweeps.
+// LB_HOT_W overrides W (8, 16) for sweeps.
 constexpr int kHotSlotsDefault = 16384;  // 64 KB of shared memory per SM (best measured on C3)
 constexpr int kHotSlotsMax = 45056;      // 176 KB
 constexpr int kHotDynMax = kHotSlotsMax * 4;
@@ -648,6 +648,30 @@ lb_status_t peers_stream_launch(lb_csr_s* A, const float* x, float* y, stream_t 
   a.x_hot = nullptr; a.hot_n4 = 0; a.x_warm = nullptr; a.cols = (int)A->cols;
   set_peers(a, pa);
   k<<<grid, W * 32, 0, s>>>(a);
+  LB_LAUNCHED();
+  return LB_OK;
+}
+
+// stream+gather ceiling probe (lb_probe_stream_gather); TIER as in the tile kernel
+template <int TIER>
+lb_status_t probe_launch(lb_csr_s* A, const float* x, stream_t s) {
+  auto k = lbk::probe_stream_gather_kernel<TIER>;
+  const int dyn = TIER >= 1 ? A->hot_n4 * 16 : 0;
+  static int conf_dyn[64] = {0};
+  static int blocks_cache[64] = {0};  // 0: not configured yet on this device
+  if (blocks_cache[A->device] == 0 || conf_dyn[A->device] != dyn) {
+    LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kHotDynMax));
+    const int pct = TIER >= 1 ? std::min(100, (int)(100.0 * (dyn + 1024.0) / (228.0 * 1024.0)) + 1) : 0;
+    LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    int blocks = 0;
+    LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, 512, dyn));
+    // with a plan: one CTA (16 warps) per SM so x_hot is staged once per SM, as in the tile kernel
+    blocks_cache[A->device] = TIER >= 1 ? 1 : std::max(1, blocks);
+    conf_dyn[A->device] = dyn;
+  }
+  const int grid = A->dev->sm_count * blocks_cache[A->device];
+  k<<<grid, 512, dyn, s>>>((int)A->nnz, TIER >= 1 ? A->hcol : A->col, A->val, x, A->x_hot, A->hot_n4, A->x_warm,
+                           (int)A->cols, 0, nullptr);
   LB_LAUNCHED();
   return LB_OK;
 }
@@ -1190,24 +1214,18 @@ lb_status_t lb_probe_stream_gather(lb_csr_t A, const float* d_x, int32_t reps, v
   if (!A || !ms_out || reps < 1 || (!d_x && A->nnz > 0)) return fail(LB_ERR_INVALID_ARG, "bad probe arguments");
   if (!A->vec32) return fail(LB_ERR_UNSUPPORTED, "probe needs 32-byte aligned col_idx/values");
   stream_t s = S(stream);
-  static int blocks_cache[64] = {0};
-  int& blocks = blocks_cache[A->device];
-  if (blocks == 0) {
-    LB_CUDA(cudaFuncSetAttribute(lbk::probe_stream_gather_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 0));
-    LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, lbk::probe_stream_gather_kernel, kNT, 0));
-    blocks = std::max(1, blocks);
-  }
-  const int grid = A->dev->sm_count * blocks;
+  const int tier = A->hot_n > 0 ? (A->warm_n > 0 ? 2 : 1) : 0;
+  lb_status_t st;
+  if (tier > 0 && (st = launch_partition_xhot(A, 0, false, d_x, s)) != LB_OK) return st;  // x_hot / x_warm of this x
+  auto launch = [&]() { return tier == 2 ? probe_launch<2>(A, d_x, s) : tier == 1 ? probe_launch<1>(A, d_x, s)
+                                                                                   : probe_launch<0>(A, d_x, s); };
+  if ((st = launch()) != LB_OK) return st;  // warm-up
   cudaEvent_t e0, e1;
   LB_CUDA(cudaEventCreate(&e0));
   LB_CUDA(cudaEventCreate(&e1));
-  lbk::probe_stream_gather_kernel<<<grid, kNT, 0, s>>>((int)A->nnz, A->col, A->val, d_x, 0, nullptr);  // warm-up
-  LB_LAUNCHED();
   LB_CUDA(cudaEventRecord(e0, s));
-  for (int r = 0; r < reps; ++r) {
-    lbk::probe_stream_gather_kernel<<<grid, kNT, 0, s>>>((int)A->nnz, A->col, A->val, d_x, 0, nullptr);
-    LB_LAUNCHED();
-  }
+  for (int r = 0; r < reps; ++r)
+    if ((st = launch()) != LB_OK) return st;
   LB_CUDA(cudaEventRecord(e1, s));
   LB_CUDA(cudaEventSynchronize(e1));
   float ms = 0.f;

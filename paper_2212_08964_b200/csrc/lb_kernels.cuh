@@ -1220,6 +1220,107 @@ __device__ __forceinline__ void tail_clear8(unsigned* p) {
   *reinterpret_cast<uint4*>(p + 4) = make_uint4(0u, 0u, 0u, 0u);
 }
 
+// Reduce one round (256 nonzeros) of tile c: products val*x summed per lane, rows that end after
+// the lane's first row end are stored directly, the ballot-based segmented scan gives each lane's
+// first row its carry-in, and `rc` (warp-uniform) carries the open row's partial to the next round.
+template <bool PEERS, typename TailT>
+__device__ __forceinline__ void stream_reduce_round(const PipeArgs& a, int4 cT, int k, int lane, bool r0e, int open_row,
+                                                    float (&val)[8], const float (&xc)[8], TailT* tail, float& rc) {
+  // (b) the row open at the tile start has no nonzero here: it ends now with the carry
+  const int i0 = cT.x;
+  if (k == 0 && r0e) {
+    if (lane == 0) put_y<PEERS>(a, i0, rc, i0 != open_row);
+    rc = 0.f;
+  }
+  // (c) positions outside the tile's nonzero range [lo, hi) add exactly zero (warp-uniform test)
+  {
+    const int lo = cT.y & 7, hi = cT.w - (cT.y & ~7);
+    if ((k == 0 && lo) || 256 * k + 256 > hi) {
+      const int q0 = 256 * k + 8 * lane;
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (q0 + e < lo || q0 + e >= hi) val[e] = 0.f;
+    }
+  }
+  // (d) reduce this round: rows that end inside the lane's 8 nonzeros after its first row end
+  // are complete; the first one waits for the carry-in from the lanes before
+  unsigned rids[8];
+  if (LB_ABL & 4) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) rids[e] = (lane == 31 && e == 7) ? 1u : 0u;
+  } else {
+    tail_read8(&tail[256 * k + 8 * lane], rids);
+  }
+  float* yt = a.y + i0 - 1;  // row r of the tile ends where rid = r + 1
+  unsigned any = 0u, first_rid = 0u;
+  float run = 0.f, first_val = 0.f;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    run = fmaf(val[e], xc[e], run);
+    const unsigned rid = rids[e];
+    any |= rid;
+    if (!(LB_ABL & 1)) put_y_if<PEERS>(a, yt, rid, i0 - 1, run, rid != 0u && first_rid != 0u);
+    const bool take = rid != 0u && first_rid == 0u;
+    first_val = take ? run : first_val;
+    first_rid = take ? rid : first_rid;
+    run = rid != 0u ? 0.f : run;
+  }
+  // segmented inclusive scan over the lanes (Kogge-Stone; a lane with a row end starts a new
+  // segment): lane l adds the partial of lane l-o unless a lane in (l-o, l] has a row end
+  const unsigned B = __ballot_sync(kFull, first_rid != 0u);
+  float v = run;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    if (LB_ABL & 2) break;
+    const float vo = __shfl_up_sync(kFull, v, o);
+    const bool reset = lane >= o ? ((B >> (lane - o + 1)) & ((1u << o) - 1u)) != 0u : true;
+    if (!reset) v = vo + v;
+  }
+  const float lval = __shfl_up_sync(kFull, v, 1);
+  const float agg_v = __shfl_sync(kFull, v, 31);
+  if (first_rid != 0u) {
+    const bool lf = (B & ((1u << lane) - 1u)) != 0u;  // a row ended in an earlier lane
+    const float carry_in = lane == 0 ? rc : (lf ? lval : rc + lval);
+    const int row = i0 - 1 + (int)first_rid;
+    if (!(LB_ABL & 1) || (LB_ABL & 4)) put_y<PEERS>(a, row, carry_in + first_val, row != open_row);
+  }
+  if (any && !(LB_ABL & 4)) tail_clear8(&tail[256 * k + 8 * lane]);
+  rc = B ? agg_v : rc + agg_v;
+}
+
+// One carry per warp (rows == a.rows for warps without tiles: skipped by the fix-up), then the
+// last CTA to finish applies all carries in warp order (Alg.3 fix-up P:332-337, deterministic).
+template <bool PEERS>
+__device__ __forceinline__ void stream_carries_fixup(const PipeArgs& a, int gw, int lane, int W, int i_last, float rc,
+                                                     int& s_last) {
+  if (lane == 0) {
+    a.carry_row[gw] = i_last;
+    a.carry_val[gw] = rc;
+  }
+  if (PEERS) __threadfence_system();  // this thread's peer stores are performed before the kernel ends
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned done = atomicAdd(a.ticket, 1u);
+    s_last = done == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    const int nc = (int)gridDim.x * W;
+    for (int c = threadIdx.x; c < nc; c += W * 32) {
+      const int r = __ldcg(a.carry_row + c);
+      if (r >= a.rows) continue;
+      if (c > 0 && __ldcg(a.carry_row + c - 1) == r) continue;
+      float sum = 0.f;
+      for (int kk = c; kk < nc && __ldcg(a.carry_row + kk) == r; ++kk) sum += __ldcg(a.carry_val + kk);
+      put_y<PEERS>(a, r, __ldcg(a.y + r) + sum);
+    }
+    if (threadIdx.x == 0) *a.ticket = 0u;
+    if (PEERS) __threadfence_system();
+  }
+}
+
 // TailT: unsigned short for merge-path tiles (<= L rows), unsigned for nonzero-split tiles (any
 // number of rows per tile).
 // TIER >= 1: the column stream is an x-reuse plan's remapped copy (lb_csr_plan_hot_x); the CTA
@@ -1288,66 +1389,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
         const bool same = k2 < R;
         stream_load(a, same ? cT : cT1, same ? k2 : k2 - R, lane, dl, spol);
       }
-      // (b) the row open at the tile start has no nonzero here: it ends now with the carry
-      const int i0 = cT.x;
-      if (k == 0 && r0e) {
-        if (lane == 0) put_y<PEERS>(a, i0, rc, i0 != open_row);
-        rc = 0.f;
-      }
-      // (c) positions outside the tile's nonzero range [lo, hi) add exactly zero (warp-uniform test)
-      {
-        const int lo = cT.y & 7, hi = cT.w - (cT.y & ~7);
-        if ((k == 0 && lo) || 256 * k + 256 > hi) {
-          const int q0 = 256 * k + 8 * lane;
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            if (q0 + e < lo || q0 + e >= hi) dc.val[e] = 0.f;
-        }
-      }
-      // (d) reduce this round: rows that end inside the lane's 8 nonzeros after its first row end
-      // are complete; the first one waits for the carry-in from the lanes before
-      unsigned rids[8];
-      if (LB_ABL & 4) {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) rids[e] = (lane == 31 && e == 7) ? 1u : 0u;
-      } else {
-        tail_read8(&tail[256 * k + 8 * lane], rids);
-      }
-      float* yt = a.y + i0 - 1;  // row r of the tile ends where rid = r + 1
-      unsigned any = 0u, first_rid = 0u;
-      float run = 0.f, first_val = 0.f;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        run = fmaf(dc.val[e], xc[e], run);
-        const unsigned rid = rids[e];
-        any |= rid;
-        if (!(LB_ABL & 1)) put_y_if<PEERS>(a, yt, rid, i0 - 1, run, rid != 0u && first_rid != 0u);
-        const bool take = rid != 0u && first_rid == 0u;
-        first_val = take ? run : first_val;
-        first_rid = take ? rid : first_rid;
-        run = rid != 0u ? 0.f : run;
-      }
-      // segmented inclusive scan over the lanes (Kogge-Stone; a lane with a row end starts a new
-      // segment): lane l adds the partial of lane l-o unless a lane in (l-o, l] has a row end
-      const unsigned B = __ballot_sync(kFull, first_rid != 0u);
-      float v = run;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        if (LB_ABL & 2) break;
-        const float vo = __shfl_up_sync(kFull, v, o);
-        const bool reset = lane >= o ? ((B >> (lane - o + 1)) & ((1u << o) - 1u)) != 0u : true;
-        if (!reset) v = vo + v;
-      }
-      const float lval = __shfl_up_sync(kFull, v, 1);
-      const float agg_v = __shfl_sync(kFull, v, 31);
-      if (first_rid != 0u) {
-        const bool lf = (B & ((1u << lane) - 1u)) != 0u;  // a row ended in an earlier lane
-        const float carry_in = lane == 0 ? rc : (lf ? lval : rc + lval);
-        const int row = i0 - 1 + (int)first_rid;
-        if (!(LB_ABL & 1) || (LB_ABL & 4)) put_y<PEERS>(a, row, carry_in + first_val, row != open_row);
-      }
-      if (any && !(LB_ABL & 4)) tail_clear8(&tail[256 * k + 8 * lane]);
-      rc = B ? agg_v : rc + agg_v;
+      stream_reduce_round<PEERS>(a, cT, k, lane, r0e, open_row, dc.val, xc, tail, rc);
       // (e) tile t done: row pass of tile t+1 (offsets prefetched), advance coords
       if (++k == R) {
         k = 0;
@@ -1373,59 +1415,44 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
     }
   }
 
-  // one carry per warp (rows == a.rows for warps without tiles: skipped by the fix-up), then the
-  // last CTA to finish applies all carries in warp order (Alg.3 fix-up, deterministic)
-  if (lane == 0) {
-    a.carry_row[gw] = i_last;
-    a.carry_val[gw] = rc;
-  }
-  if (PEERS) __threadfence_system();  // this thread's peer stores are performed before the kernel ends
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    const unsigned done = atomicAdd(a.ticket, 1u);
-    s_last = done == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (s_last) {
-    __threadfence();
-    const int nc = (int)gridDim.x * W;
-    for (int c = threadIdx.x; c < nc; c += W * 32) {
-      const int r = __ldcg(a.carry_row + c);
-      if (r >= a.rows) continue;
-      if (c > 0 && __ldcg(a.carry_row + c - 1) == r) continue;
-      float sum = 0.f;
-      for (int kk = c; kk < nc && __ldcg(a.carry_row + kk) == r; ++kk) sum += __ldcg(a.carry_val + kk);
-      put_y<PEERS>(a, r, __ldcg(a.y + r) + sum);
-    }
-    if (threadIdx.x == 0) *a.ticket = 0u;
-    if (PEERS) __threadfence_system();
-  }
+  stream_carries_fixup<PEERS>(a, gw, lane, W, i_last, rc, s_last);
 }
 
 // ----------------------------------------------------------------------------- ceiling probe
 // Diagnostic: stream col/val with the tile kernels' 256-bit loads and gather x[col] with no row
 // structure (no scans, no y) -- the stream+gather ceiling of this matrix on this GPU, against which
 // bench.py reports the tile processor.  `flag` is 0 at run time (keeps the sum live).
-__global__ void __launch_bounds__(256) probe_stream_gather_kernel(int nnz, const int* __restrict__ col,
+// TIER >= 1: the column stream is an x-reuse plan's (hot slots ~s, warm cols + w) and the CTA stages
+// x_hot in dynamic shared memory exactly as merge_stream_kernel does -- the ceiling of the plan.
+template <int TIER>
+__global__ void __launch_bounds__(512) probe_stream_gather_kernel(int nnz, const int* __restrict__ col,
                                                                   const float* __restrict__ val,
-                                                                  const float* __restrict__ x, int flag,
-                                                                  float* sink) {
+                                                                  const float* __restrict__ x,
+                                                                  const float* __restrict__ x_hot, int hot_n4,
+                                                                  const float* __restrict__ x_warm, int cols,
+                                                                  int flag, float* sink) {
+  extern __shared__ __align__(16) float s_xhot[];
   const uint64_t pol = policy_evict_first();
+  const uint64_t xpol = TIER == 2 ? policy_evict_last() : 0ull;
+  if (TIER >= 1) {
+    for (int i = threadIdx.x; i < hot_n4; i += blockDim.x)
+      reinterpret_cast<float4*>(s_xhot)[i] = __ldcg(reinterpret_cast<const float4*>(x_hot) + i);
+    __syncthreads();
+  }
+  const uint32_t sxb = TIER >= 1 ? (uint32_t)__cvta_generic_to_shared(s_xhot) : 0u;
   float s = 0.f;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * 8;
   int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
   for (; i + 8 <= nnz; i += stride) {
-    int c[8];
-    float v[8], xv[8];
-    ld_stream_v8(col + i, c, pol);
-    ld_stream_v8(val + i, v, pol);
+    StreamRound d;
+    float xv[8];
+    ld_stream_v8(col + i, d.col, pol);
+    ld_stream_v8(val + i, d.val, pol);
+    gx8<false, TIER>(x, x_warm, cols, sxb, d, xv, xpol, pol);
 #pragma unroll
-    for (int e = 0; e < 8; ++e) xv[e] = ld_x(x + c[e]);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) s = fmaf(v[e], xv[e], s);
+    for (int e = 0; e < 8; ++e) s = fmaf(d.val[e], xv[e], s);
   }
-  for (; i < nnz; ++i) s = fmaf(val[i], x[col[i]], s);
+  for (; i < nnz; ++i) s = fmaf(val[i], gx<false, TIER>(x, x_warm, cols, sxb, col[i], xpol, pol), s);
   if (flag) sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
