@@ -46,6 +46,7 @@ def lib():
         L.oracle_partition_nz.argtypes = [i64, i64, p, i64, p]
         L.oracle_partition_nz.restype = i64
         L.oracle_shard_bounds.argtypes = [i64, p, ctypes.c_int32, p]
+        L.oracle_bins.argtypes = [i64, p, i64, i64, p, p]
         L.oracle_x_plan.argtypes = [i64, i64, p, ctypes.c_int32, i64, p, p, p, p, p, p, p, p]
         L.oracle_x_plan.restype = i64
         L.oracle_sssp.argtypes = [i64, p, p, p, i64, p, p]
@@ -138,6 +139,17 @@ def shard_bounds(row_offsets, G: int) -> np.ndarray:
     out = np.empty(G + 1, np.int64)
     lib().oracle_shard_bounds(off.size - 1, _ptr(off), G, _ptr(out))
     return out
+
+
+def bins(row_offsets, block_size: int = 256, warp_size: int = 32):
+    """Alg.4 three-bin classification (oracle_bins): (cta_rows, warp_rows, thread_rows), ascending int32."""
+    off = _np(row_offsets, np.int32)
+    rows = off.size - 1
+    ids = np.zeros(max(rows, 1), np.int32)
+    sizes = np.zeros(3, np.int64)
+    lib().oracle_bins(rows, _ptr(off), block_size, warp_size, _ptr(ids), _ptr(sizes))
+    n0, n1 = int(sizes[0]), int(sizes[1])
+    return ids[:n0].copy(), ids[n0:n0 + n1].copy(), ids[n0 + n1:rows].copy()
 
 
 def num_threads() -> int:

@@ -199,6 +199,28 @@ void oracle_shard_bounds(int64_t rows, const int32_t *row_offsets, int32_t G, in
 }
 
 /*
+ * Three-bin classification of the binning schedule (Alg.4 P:364-377 [Sec. Binning and
+ * Reordering]): num_nonzeros = offsets[row+1] - offsets[row]; >= block_size -> CTA bin, else
+ * >= warp_size -> warp bin, else thread bin.  Each bin lists its rows in ascending order (reading
+ * R21: Alg.4 appends with bin_size++ in an unspecified order).  Output layout of ids:
+ * [CTA bin | warp bin | thread bin]; sizes[0..2] = bin sizes.  One pass per bin over the rows.
+ */
+void oracle_bins(int64_t rows, const int32_t *row_offsets, int64_t block_size, int64_t warp_size,
+                 int32_t *ids, int64_t *sizes)
+{
+    int64_t n = 0;
+    for (int bin = 0; bin < 3; ++bin) {
+        int64_t start = n;
+        for (int64_t r = 0; r < rows; ++r) {
+            int64_t num_nonzeros = (int64_t)row_offsets[r + 1] - row_offsets[r];
+            int b = num_nonzeros >= block_size ? 0 : (num_nonzeros >= warp_size ? 1 : 2);
+            if (b == bin) ids[n++] = (int32_t)r;
+        }
+        sizes[bin] = n - start;
+    }
+}
+
+/*
  * x-reuse plan by definition (B200 extension of the merge-path tile processor -- DESIGN.md section 6b
  * and include/lb.h lb_csr_plan_hot_x; the paper has no such step: it only fixes that the tile
  * processor gathers x[col] per nonzero, Listing 3).

@@ -537,3 +537,58 @@ def test_sssp_unit_weights_are_bfs_levels():
         frontier = sorted(nxt)
     got = oracle.sssp(off, col, np.ones(col.size, np.float32), 0)
     assert np.array_equal(got, level)
+
+
+# ---------------------------------------------------------------- binning (Alg.4) pins
+
+BIN_GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "binning_examples.json")
+
+
+def test_bins_worked_examples():
+    """Hand-derived bins on both sides of each threshold (tests/golden/binning_examples.json)."""
+    with open(BIN_GOLDEN) as f:
+        ex = json.load(f)["examples"]
+    for e in ex:
+        off = np.concatenate([[0], np.cumsum(e["lengths"])]).astype(np.int32)
+        cta, warp, thread = oracle.bins(off, e["block_size"], e["warp_size"])
+        assert cta.tolist() == e["cta"] and warp.tolist() == e["warp"] and thread.tolist() == e["thread"], e
+
+
+@pytest.mark.parametrize("gen", ["rmat", "stencil", "skewed", "uniform", "random"])
+def test_bins_invariants_and_counts(gen):
+    """The bins partition the rows, each bin is ascending, every row satisfies its bin's predicate, and
+    the bin sizes equal an independent histogram of the row lengths (np.digitize + bincount)."""
+    if gen == "random":
+        A = random_csr(np.random.default_rng(5), 3000, 500, 600, 0.3, "int")
+    else:
+        A = {"rmat": lambda: lbgen.rmat(11, 16, 3, "int"), "stencil": lambda: lbgen.stencil(40, 2, "int"),
+             "skewed": lambda: lbgen.skewed(4096, 10, 3000, 60000, 4, "int"),
+             "uniform": lambda: lbgen.uniform(500, 0.2, 1, "int")}[gen]()
+    off = A.row_offsets.numpy().astype(np.int64)
+    lens = np.diff(off)
+    cta, warp, thread = oracle.bins(A.row_offsets, 256, 32)
+    allr = np.concatenate([cta, warp, thread])
+    assert np.array_equal(np.sort(allr), np.arange(A.rows))
+    for b in (cta, warp, thread):
+        assert np.all(np.diff(b) > 0)
+    assert np.all(lens[cta] >= 256) and np.all((lens[warp] >= 32) & (lens[warp] < 256)) and np.all(lens[thread] < 32)
+    hist = np.bincount(np.digitize(lens, [32, 256]), minlength=3)  # 0: < 32, 1: [32, 256), 2: >= 256
+    assert (thread.size, warp.size, cta.size) == tuple(hist)
+
+
+def test_bins_closed_forms():
+    """Special cases fixed by construction: a stencil's rows (<= 5 nonzeros) are all thread-binned; the
+    skewed generator's giant rows (3000 nonzeros) are exactly the CTA bin and its other rows (< 32) the
+    thread bin; the identity matrix is all thread bin; an empty matrix has three empty bins."""
+    S = lbgen.stencil(30, 2, "int")
+    c, w, t = oracle.bins(S.row_offsets)
+    assert c.size == 0 and w.size == 0 and np.array_equal(t, np.arange(S.rows))
+    K = lbgen.skewed(4096, 10, 3000, 60000, 4, "int")
+    lens = np.diff(K.row_offsets.numpy())
+    c, w, t = oracle.bins(K.row_offsets)
+    assert np.array_equal(c, np.flatnonzero(lens == 3000)) and c.size == 10 and w.size == 0
+    assert t.size == K.rows - 10
+    c, w, t = oracle.bins(np.arange(65, dtype=np.int32))
+    assert c.size == 0 and w.size == 0 and np.array_equal(t, np.arange(64))
+    c, w, t = oracle.bins(np.zeros(1, np.int32))
+    assert c.size == w.size == t.size == 0
