@@ -69,6 +69,13 @@ typedef enum {
  *                  1016 nonzeros, each tile's first row found by a 1-D binary search of
  *                  row_offsets (lb_partition_nz); rows without nonzeros cost no work, so tiles may
  *                  span arbitrarily many empty rows.  Runs on the merge-path tile processor.
+ *  WARP_MAPPED     warp-level load balancing: every warp takes an equal share of rows
+ *                  (a contiguous run) and processes them one at a time, the 32 lanes striding the
+ *                  row's atoms by 32 ("CSR-vector"); fixed xor-tree sum over the lanes.
+ *  BINNING         three-bin schedule (Alg.4; three kernels): rows with >= 256
+ *                  nonzeros are processed by a CTA each, rows with >= 32 by a warp each, the rest by
+ *                  a thread each; the bins are rebuilt on the device in every call (count, scan,
+ *                  stable scatter -- ascending row ids per bin, reading R21), no host sync.
  *  AUTO            the paper's heuristic: merge-path unless (rows < alpha or cols < alpha)
  *                  and nnz < beta (alpha = 500, beta = 10000), then thread-mapped; extended with a
  *                  row-regularity test for B200 (reading R18): thread-mapped when the longest row
@@ -81,7 +88,9 @@ typedef enum {
   LB_SCHED_MERGE_PATH = 2,
   LB_SCHED_BLOCK_MAPPED = 3,
   LB_SCHED_AUTO = 4,
-  LB_SCHED_NONZERO_SPLIT = 5
+  LB_SCHED_NONZERO_SPLIT = 5,
+  LB_SCHED_WARP_MAPPED = 6,
+  LB_SCHED_BINNING = 7
 } lb_schedule_t;
 
 
@@ -235,6 +244,16 @@ lb_status_t lb_csr_hot_plan(lb_csr_t A, int32_t* hot_n, int64_t* hot_nnz, int64_
  * before the first round), a bad source or a non-square matrix.
  */
 lb_status_t lb_sssp(lb_csr_t A, int64_t source, lb_schedule_t sched, float* d_dist, void* stream, int32_t* rounds_out);
+
+/*
+ * lb_bins -- the three bins of the BINNING schedule (Alg.4): rows with >= 256 nonzeros
+ * (CTA bin), >= 32 (warp bin), the rest (thread bin), each in ascending row order (reading R21).
+ *  d_ids     int32[rows] device (output): [CTA bin | warp bin | thread bin].
+ *  h_sizes   int64[3] host (output): the bin sizes.
+ * Synchronises `stream` once (to read the sizes).  Allocates the handle's binning workspace
+ * (4*rows bytes + 12 bytes per 1024 rows) on first use.
+ */
+lb_status_t lb_bins(lb_csr_t A, int32_t* d_ids, int64_t h_sizes[3], void* stream);
 
 /* Flags for lb_spmv_ex. */
 #define LB_SPMV_REPARTITION 1u /* MERGE_PATH: recompute the partition inside this call */

@@ -274,6 +274,11 @@ struct lb_csr_s {
   int* fo = nullptr;           // [rows + 1] frontier degree prefix (merge-path)
   int* bsum = nullptr;         // [rows / kScanChunk + 2] scan block sums
   int* counts = nullptr;       // [4] frontier size, next size, negative-weight flag
+  // BINNING workspace (allocated on first use): [CTA | warp | thread] bin row ids, per-block counts
+  void* bin_mem = nullptr;
+  int* bin_ids = nullptr;      // [rows]
+  int* bin_counts = nullptr;   // [3 * nb] counts, then write offsets
+  int* bin_sizes = nullptr;    // [3]
 };
 
 namespace {
@@ -872,6 +877,42 @@ lb_status_t select_schedule(lb_csr_s* A, stream_t s, lb_schedule_t* out) {
   return LB_OK;
 }
 
+constexpr int kWarpRows = 4;  // WARP_MAPPED: rows per warp
+
+// BINNING (Alg.4): build the three bins on the device (stable compaction; no host sync)
+lb_status_t launch_bins(lb_csr_s* A, stream_t s) {
+  const int nb = (int)((A->rows + lbk::kBinRows - 1) / lbk::kBinRows);
+  if (!A->bin_mem) {
+    const size_t bytes = align256((size_t)A->rows * 4) + align256((size_t)3 * nb * 4) + align256(16);
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) { cudaGetLastError(); return fail(LB_ERR_OOM, "binning workspace"); }
+    char* q = static_cast<char*>(p);
+    A->bin_mem = p;
+    A->bin_ids = reinterpret_cast<int*>(q); q += align256((size_t)A->rows * 4);
+    A->bin_counts = reinterpret_cast<int*>(q); q += align256((size_t)3 * nb * 4);
+    A->bin_sizes = reinterpret_cast<int*>(q);
+  }
+  lbk::bin_count_kernel<<<nb, 256, 0, s>>>((int)A->rows, A->off, nb, A->bin_counts);
+  LB_LAUNCHED();
+  lbk::bin_scan_kernel<<<1, 1024, 0, s>>>(nb, A->bin_counts, A->bin_sizes);
+  LB_LAUNCHED();
+  lbk::bin_scatter_kernel<<<nb, 256, 0, s>>>((int)A->rows, A->off, nb, A->bin_counts, A->bin_ids);
+  LB_LAUNCHED();
+  return LB_OK;
+}
+
+// the three bin kernels (one specialised kernel per bin), persistent grids
+lb_status_t launch_bin_kernels(lb_csr_s* A, const float* x, float* y, stream_t s) {
+  const int sms = A->dev->sm_count;
+  lbk::bin_cta_kernel<<<sms * 8, 256, 0, s>>>(A->bin_ids, A->bin_sizes, A->off, A->col, A->val, x, y);
+  LB_LAUNCHED();
+  lbk::bin_warp_kernel<<<sms * 8, 256, 0, s>>>(A->bin_ids, A->bin_sizes, A->off, A->col, A->val, x, y);
+  LB_LAUNCHED();
+  lbk::bin_thread_kernel<<<sms * 16, 256, 0, s>>>(A->bin_ids, A->bin_sizes, A->off, A->col, A->val, x, y);
+  LB_LAUNCHED();
+  return LB_OK;
+}
+
 lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y, uint32_t flags, stream_t s,
                       PhaseEvents* pe, const PeerArgs* pa = nullptr, bool* fused = nullptr) {
   if (fused) *fused = false;
@@ -948,6 +989,25 @@ lb_status_t spmv_impl(lb_csr_s* A, lb_schedule_t sched, const float* x, float* y
         case 4088: return launch_merge<4088>(A, x, y, s, pe);
         default: return fail(LB_ERR_INVALID_ARG, "unsupported tile length %d", A->L);
       }
+    }
+    case LB_SCHED_WARP_MAPPED: {
+      if (pe) LB_CUDA(cudaEventRecord(pe->ev[1], s));
+      // an equal share of rows per warp, kWarpRows rows each, with the warps
+      // oversubscribed so that the hardware scheduler absorbs the imbalance
+      const int64_t rpw = kWarpRows;
+      const int64_t grid = ((A->rows + rpw - 1) / rpw * 32 + kNT - 1) / kNT;
+      lbk::warp_mapped_kernel<<<(unsigned)grid, kNT, 0, s>>>((int)A->rows, (int)rpw, A->off, A->col, A->val, x, y);
+      LB_LAUNCHED();
+      if (pe) { LB_CUDA(cudaEventRecord(pe->ev[2], s)); LB_CUDA(cudaEventRecord(pe->ev[3], s)); }
+      return LB_OK;
+    }
+    case LB_SCHED_BINNING: {
+      lb_status_t st;
+      if ((st = launch_bins(A, s)) != LB_OK) return st;  // bins depend only on A, rebuilt every call (Alg.4 runtime phase)
+      if (pe) LB_CUDA(cudaEventRecord(pe->ev[1], s));
+      if ((st = launch_bin_kernels(A, x, y, s)) != LB_OK) return st;
+      if (pe) { LB_CUDA(cudaEventRecord(pe->ev[2], s)); LB_CUDA(cudaEventRecord(pe->ev[3], s)); }
+      return LB_OK;
     }
     case LB_SCHED_NONZERO_SPLIT: {
       if (!A->vec32) return fail(LB_ERR_UNSUPPORTED, "nonzero-split needs 32-byte aligned col_idx/values");
@@ -1124,6 +1184,8 @@ const char* lb_kernel_name(lb_csr_t A, lb_schedule_t sched) {
     case LB_SCHED_GROUP_MAPPED: return "group_mapped_kernel<32>";
     case LB_SCHED_BLOCK_MAPPED: return "group_mapped_kernel<256>";
     case LB_SCHED_NONZERO_SPLIT: return "partition_nz_kernel + merge_stream_kernel<8,4,2,u32>";
+    case LB_SCHED_WARP_MAPPED: return "warp_mapped_kernel";
+    case LB_SCHED_BINNING: return "bin_{count,scan,scatter}_kernel + bin_{cta,warp,thread}_kernel";
     case LB_SCHED_MERGE_PATH: {
       if (!A || l_index(A->L) < 0) return "";
       if (hot_usable(A)) {
@@ -1175,11 +1237,28 @@ lb_status_t lb_csr_create(int64_t rows, int64_t cols, int64_t nnz, const int32_t
   return LB_OK;
 }
 
+lb_status_t lb_bins(lb_csr_t A, int32_t* d_ids, int64_t h_sizes[3], void* stream) {
+  g_err.clear();
+  if (!A || !h_sizes || (!d_ids && A->rows > 0)) return fail(LB_ERR_INVALID_ARG, "bad lb_bins arguments");
+  h_sizes[0] = h_sizes[1] = h_sizes[2] = 0;
+  if (A->rows == 0) return LB_OK;
+  stream_t s = S(stream);
+  lb_status_t st;
+  if ((st = launch_bins(A, s)) != LB_OK) return st;
+  LB_CUDA(cudaMemcpyAsync(d_ids, A->bin_ids, (size_t)A->rows * 4, cudaMemcpyDeviceToDevice, s));
+  int h[3];
+  LB_CUDA(cudaMemcpyAsync(h, A->bin_sizes, sizeof h, cudaMemcpyDeviceToHost, s));
+  LB_CUDA(cudaStreamSynchronize(s));
+  for (int q = 0; q < 3; ++q) h_sizes[q] = h[q];
+  return LB_OK;
+}
+
 lb_status_t lb_csr_destroy(lb_csr_t A) {
   if (!A) return LB_OK;
   if (A->owns_scratch && A->coords) cudaFree(A->coords);
   if (A->plan_mem) cudaFree(A->plan_mem);
   if (A->sssp_mem) cudaFree(A->sssp_mem);
+  if (A->bin_mem) cudaFree(A->bin_mem);
   delete A;
   return LB_OK;
 }

@@ -2233,4 +2233,205 @@ __global__ void __launch_bounds__(256) group_mapped_kernel(int rows, const int* 
   }
 }
 
+// ----------------------------------------------------------------------------- warp-mapped
+// Warp-level load balancing (P:1031-1034 [Sec. Warp- and block-level load balancing]): every warp
+// takes an equal share of tiles (rows) -- a contiguous run of ceil(rows / warps) rows -- and
+// processes them one at a time; the atoms of a row are processed in parallel by the 32 lanes, each
+// striding by the warp size ("CSR-vector").  Lane l sums k = b+l, b+l+32, ... in order; the row
+// sum is a fixed xor-shuffle tree over the lanes (deterministic).
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float row_dot_lanes(int b, int e, int lane, int stride, const int* __restrict__ col,
+                                               const float* __restrict__ val, const float* __restrict__ x) {
+  float s0 = 0.f, s1 = 0.f;
+  int k = b + lane;
+  for (; k + stride < e; k += 2 * stride) {
+    s0 = fmaf(__ldg(val + k), ld_x(x + __ldg(col + k)), s0);
+    s1 = fmaf(__ldg(val + k + stride), ld_x(x + __ldg(col + k + stride)), s1);
+  }
+  if (k < e) s0 = fmaf(__ldg(val + k), ld_x(x + __ldg(col + k)), s0);
+  return s0 + s1;
+}
+
+__global__ void __launch_bounds__(256) warp_mapped_kernel(int rows, int rows_per_warp, const int* __restrict__ off,
+                                                          const int* __restrict__ col, const float* __restrict__ val,
+                                                          const float* __restrict__ x, float* __restrict__ y) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t r0 = w * rows_per_warp;
+  const int64_t r1 = (r0 + rows_per_warp < rows ? r0 + rows_per_warp : (int64_t)rows);
+  for (int64_t r = r0; r < r1; ++r) {
+    const float s = warp_sum(row_dot_lanes(__ldg(off + r), __ldg(off + r + 1), lane, 32, col, val, x));
+    if (lane == 0) y[r] = s;
+  }
+}
+
+// ----------------------------------------------------------------------------- binning
+// Three-bin schedule (Alg.4 P:341-397 [Sec. Binning and Reordering]; three kernels): rows
+// with >= kBinCta nonzeros go to the CTA bin, >= kBinWarp to the warp bin, the rest to the thread
+// bin.  The bins are built by a stable compaction (count per block of
+// kBinRows rows -> one-block scan -> scatter), so each bin lists its rows in ascending order
+// (reading R21; Alg.4's atomic bin_size++ leaves the order unspecified).  Layout of `ids`:
+// [CTA bin | warp bin | thread bin], sizes in sizes[0..2].  The three processing kernels are
+// persistent and read the bin sizes on the device, so the whole schedule needs no host sync.
+constexpr int kBinCta = 256;   // block_size (threads per CTA of the CTA-bin kernel)
+constexpr int kBinWarp = 32;   // warp_size
+constexpr int kBinRows = 1024; // rows per compaction block (256 threads x 4)
+
+__device__ __forceinline__ int bin_of(int n) { return n >= kBinCta ? 0 : n >= kBinWarp ? 1 : 2; }
+
+// counts[bin * nb + blk] = rows of block blk in `bin`
+__global__ void __launch_bounds__(256) bin_count_kernel(int rows, const int* __restrict__ off, int nb,
+                                                        int* __restrict__ counts) {
+  __shared__ int s_c[3];
+  if (threadIdx.x < 3) s_c[threadIdx.x] = 0;
+  __syncthreads();
+  int c[3] = {0, 0, 0};
+  const int64_t r0 = (int64_t)blockIdx.x * kBinRows;
+  for (int i = threadIdx.x; i < kBinRows; i += 256) {
+    const int64_t r = r0 + i;
+    if (r < rows) {
+      const int b = bin_of(__ldg(off + r + 1) - __ldg(off + r));
+      c[0] += b == 0; c[1] += b == 1; c[2] += b == 2;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    int v = c[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_c[q], v);
+  }
+  __syncthreads();
+  if (threadIdx.x < 3) counts[threadIdx.x * nb + blockIdx.x] = s_c[threadIdx.x];
+}
+
+// exclusive scan of counts (in place, bin-major so that bin q's blocks follow bin q-1's: the
+// result is each block's write offset into `ids`), sizes[q] = rows in bin q
+__global__ void __launch_bounds__(1024) bin_scan_kernel(int nb, int* __restrict__ counts, int* __restrict__ sizes) {
+  __shared__ int s_w[32];
+  __shared__ int s_carry;
+  if (threadIdx.x == 0) s_carry = 0;
+  __syncthreads();
+  const int n = 3 * nb;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int base = 0; base < n; base += 1024) {
+    const int i = base + threadIdx.x;
+    const int v = i < n ? counts[i] : 0;
+    int incl = warp_incl_scan_int(v, lane);
+    if (lane == 31) s_w[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+      const int t = s_w[lane];
+      s_w[lane] = warp_incl_scan_int(t, lane) - t;
+    }
+    __syncthreads();
+    const int excl = s_carry + s_w[warp] + incl - v;
+    if (i < n) counts[i] = excl;
+    __syncthreads();
+    if (threadIdx.x == 1023) s_carry = excl + v;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    // sizes from the offsets of each bin's first block and the total
+    const int o1 = nb > 0 ? counts[nb] : 0, o2 = nb > 0 ? counts[2 * nb] : 0;
+    sizes[0] = o1;
+    sizes[1] = o2 - o1;
+    sizes[2] = s_carry - o2;
+  }
+}
+
+// ids[offset of (bin, block) + rank of the row among the block's rows of that bin] = row
+__global__ void __launch_bounds__(256) bin_scatter_kernel(int rows, const int* __restrict__ off, int nb,
+                                                          const int* __restrict__ offsets, int* __restrict__ ids) {
+  __shared__ int s_w[3][8];
+  __shared__ int s_base[3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < 3) s_base[threadIdx.x] = offsets[threadIdx.x * nb + blockIdx.x];
+  __syncthreads();
+  // 4 rounds of 256 consecutive rows; within a round rows are ranked in thread order
+  for (int rd = 0; rd < kBinRows / 256; ++rd) {
+    const int64_t r = (int64_t)blockIdx.x * kBinRows + rd * 256 + threadIdx.x;
+    const int b = r < rows ? bin_of(__ldg(off + r + 1) - __ldg(off + r)) : 3;
+    int rank = 0;
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const unsigned m = __ballot_sync(kFull, b == q);
+      if (lane == 0) s_w[q][warp] = __popc(m);
+      if (b == q) rank = __popc(m & ((1u << lane) - 1u));
+    }
+    __syncthreads();
+    if (b < 3) {
+      int before = 0;
+      for (int w = 0; w < warp; ++w) before += s_w[b][w];
+      ids[s_base[b] + before + rank] = (int)r;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+      int t = 0;
+      for (int w = 0; w < 8; ++w) t += s_w[threadIdx.x][w];
+      s_base[threadIdx.x] += t;
+    }
+    __syncthreads();
+  }
+}
+
+// CTA bin: one CTA (256 threads) per row, threads stride the row by 256, fixed-order block sum
+__global__ void __launch_bounds__(256) bin_cta_kernel(const int* __restrict__ ids, const int* __restrict__ sizes,
+                                                      const int* __restrict__ off, const int* __restrict__ col,
+                                                      const float* __restrict__ val, const float* __restrict__ x,
+                                                      float* __restrict__ y) {
+  __shared__ float s_w[8];
+  const int n = __ldg(sizes + 0);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const int r = __ldg(ids + i);
+    const float v = warp_sum(row_dot_lanes(__ldg(off + r), __ldg(off + r + 1), threadIdx.x, 256, col, val, x));
+    if (lane == 0) s_w[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float s = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) s += s_w[w];
+      y[r] = s;
+    }
+    __syncthreads();
+  }
+}
+
+// warp bin: one warp per row, lanes stride by 32
+__global__ void __launch_bounds__(256) bin_warp_kernel(const int* __restrict__ ids, const int* __restrict__ sizes,
+                                                       const int* __restrict__ off, const int* __restrict__ col,
+                                                       const float* __restrict__ val, const float* __restrict__ x,
+                                                       float* __restrict__ y) {
+  const int n0 = __ldg(sizes + 0), n = __ldg(sizes + 1);
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < n; i += nw) {
+    const int r = __ldg(ids + n0 + i);
+    const float s = warp_sum(row_dot_lanes(__ldg(off + r), __ldg(off + r + 1), lane, 32, col, val, x));
+    if (lane == 0) y[r] = s;
+  }
+}
+
+// thread bin: one thread per row, atoms summed sequentially (Alg.4 THREAD_BIN; reading R21 for
+// its y[A.indices[k]] garble: the row's own y[row] is written)
+__global__ void __launch_bounds__(256) bin_thread_kernel(const int* __restrict__ ids, const int* __restrict__ sizes,
+                                                         const int* __restrict__ off, const int* __restrict__ col,
+                                                         const float* __restrict__ val, const float* __restrict__ x,
+                                                         float* __restrict__ y) {
+  const int base = __ldg(sizes + 0) + __ldg(sizes + 1), n = __ldg(sizes + 2);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int r = __ldg(ids + base + i);
+    const int b = __ldg(off + r), e = __ldg(off + r + 1);
+    float s = 0.f;
+    for (int k = b; k < e; ++k) s = fmaf(__ldg(val + k), ld_x(x + __ldg(col + k)), s);
+    y[r] = s;
+  }
+}
+
 }  // namespace lbk

@@ -20,7 +20,7 @@ HEADER = os.path.join(_ROOT, "include", "lb.h")
 
 LB_OK, LB_ERR_INVALID_ARG, LB_ERR_INVALID_CSR, LB_ERR_UNSUPPORTED, LB_ERR_OOM, LB_ERR_CUDA, LB_ERR_NCCL = range(7)
 SCHEDULES = {"thread_mapped": 0, "group_mapped": 1, "merge_path": 2, "block_mapped": 3, "auto": 4,
-             "nonzero_split": 5}
+             "nonzero_split": 5, "warp_mapped": 6, "binning": 7}
 SCHEDULE_NAMES = {v: k for k, v in SCHEDULES.items()}
 LB_SPMV_REPARTITION = 1
 DEFAULT_ITEMS_PER_TILE = 1016
@@ -72,6 +72,7 @@ def lib() -> ctypes.CDLL:
         "lb_csr_hot_plan": ([p, ctypes.POINTER(i32), ctypes.POINTER(i64), ctypes.POINTER(i64), ctypes.POINTER(i64),
                              p, p, p, p], st),
         "lb_sssp": ([p, i64, ctypes.c_int, p, p, ctypes.POINTER(i32)], st),
+        "lb_bins": ([p, p, ctypes.POINTER(i64), p], st),
         "lb_spmv_host_workspace_size": ([i64, i64, i64], sz),
         "lb_spmv_host": ([i64, i64, i64, p, p, p, p, p, ctypes.c_int, p, sz, p], st),
         "lb_spmv_phase_times": ([p, ctypes.c_int, p, p, p, ctypes.POINTER(ctypes.c_float)], st),
@@ -295,6 +296,14 @@ class CsrMatrix:
                                      None, None, None, None))
         return {"hot_cols": int(n.value), "hot_nnz": int(h.value), "warm_cols": int(wn.value),
                 "warm_nnz": int(wh.value)}
+
+    def bins(self, stream=None):
+        """The BINNING schedule's three bins (lb_bins): (cta_rows, warp_rows, thread_rows), ascending int32."""
+        ids = torch.empty(self.rows, dtype=torch.int32, device=self.row_offsets.device)
+        sizes = (ctypes.c_int64 * 3)()
+        _check(lib().lb_bins(self.handle, ids.data_ptr() if self.rows else None, sizes, _stream(stream)))
+        n0, n1 = int(sizes[0]), int(sizes[1])
+        return ids[:n0], ids[n0:n0 + n1], ids[n0 + n1:]
 
     def hot_plan(self, stream=None):
         """Copies of the plan's hot slot table, warm table and remapped column stream (None without a plan)."""

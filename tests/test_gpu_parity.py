@@ -20,7 +20,8 @@ import paper_2212_08964_b200 as lb
 
 pytestmark = pytest.mark.gpu
 
-SCHEDS = ["merge_path", "thread_mapped", "group_mapped", "block_mapped", "auto", "nonzero_split"]
+SCHEDS = ["merge_path", "thread_mapped", "group_mapped", "block_mapped", "auto", "nonzero_split", "warp_mapped",
+          "binning"]
 TOL = 1e-5
 
 
@@ -396,6 +397,39 @@ def test_every_merge_variant(variant, L, monkeypatch):
         x = torch.ones(A.cols)
         y_ref, s_ref = ref(A, x)
         check_y(run(A, x, "merge_path", L), y_ref, s_ref, True, f"v{variant}/{name}")
+
+
+# ---------------------------------------------------------------- binning (Alg.4, NEXT-3)
+
+def _check_bins(A: lbgen.Csr, what: str):
+    M = lb.CsrMatrix.from_csr(A, device="cuda")
+    got = [b.cpu().numpy() for b in M.bins()]
+    want = oracle.bins(A.row_offsets.cpu())
+    for g, w, name in zip(got, want, ("cta", "warp", "thread")):
+        assert np.array_equal(g, w), f"{what}: {name} bin differs ({g.size} vs {w.size} rows)"
+
+
+def test_bins_bit_exact():
+    """lb_bins (the BINNING schedule's device-built bins) equal oracle_bins exactly: generators whose rows
+    fall in all three bins, ragged random matrices spanning many compaction blocks (1024 rows) with a
+    ragged tail, and the edge cases (one row, all-empty rows, thresholds 31/32 and 255/256)."""
+    rng = np.random.default_rng(21)
+    cases = {"rmat": lbgen.rmat(14, 16, 5, "int"), "skewed": lbgen.skewed(1 << 13, 7, 5000, 90_000, 8, "int"),
+             "stencil": lbgen.stencil(90, 2, "int"), "random": random_csr(rng, 5000, 700, 700, 0.4, "int"),
+             "one_row": _csr([0, 300], 5), "empty_rows": _csr([0] * 2050, 4),
+             "thresholds": _csr([0, 31, 63, 318, 574, 574], 9)}
+    for name, A in cases.items():
+        _check_bins(A, name)
+
+
+@pytest.mark.parametrize("cfg", ["c3", "c4"])
+def test_bins_full_size(cfg):
+    """The bins at BASELINE.json sizes (C3: all three bins populated; C4: the 1,000 giant rows)."""
+    torch.cuda.empty_cache()
+    A = lbgen.make_config(cfg, "int", device="cuda")
+    _check_bins(A, cfg)
+    del A
+    torch.cuda.empty_cache()
 
 
 # ---------------------------------------------------------------- AUTO schedule (P:1149 + reading R18)

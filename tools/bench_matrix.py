@@ -7,7 +7,7 @@ import lbgen
 import paper_2212_08964_b200 as lb
 
 CFGS = sys.argv[1].split(",") if len(sys.argv) > 1 else ["c1", "c2", "c3", "c4", "c5"]
-SCHEDS = ["merge_path", "nonzero_split", "thread_mapped", "group_mapped", "block_mapped", "auto"]
+SCHEDS = ["merge_path", "nonzero_split", "thread_mapped", "group_mapped", "block_mapped", "warp_mapped", "binning", "auto"]
 
 
 def timeit(fn, n):
