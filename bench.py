@@ -114,7 +114,7 @@ class ClockSampler:
 
     def summary(self):
         if not self.out:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no nvidia-smi samples"], "samples": 0}
         rows = []
         for ln in self.out.strip().splitlines():
             f = [c.strip() for c in ln.split(",")]
@@ -409,6 +409,12 @@ def run_multi(args, cfg):
     sampler = ClockSampler(local) if (rank == 0 and not args.no_extras) else None
     if sampler:
         sampler.__enter__()
+    if not args.no_extras:
+        # soak (every rank, same count) so the sampler sees steady-state clocks even if K steps are short
+        n_soak = max(1, int(1000.0 / max(ms_np if no_plan else 1.0, 0.05)))
+        for _ in range(n_soak):
+            step()
+        torch.cuda.synchronize()
     n0 = lb.launch_count()
     dist.barrier()
     torch.cuda.synchronize()
@@ -432,9 +438,33 @@ def run_multi(args, cfg):
     f1.record(stream)
     torch.cuda.synchronize()
     spmv_ms_local = f0.elapsed_time(f1) / args.steps
-    t = torch.tensor([ms_local, spmv_ms_local], device=dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms, spmv_ms = float(t[0]), float(t[1])
+    # e2e through the public API: every step copies this rank's shard (CSR arrays) and x from pinned
+    # host memory into the handle's borrowed arrays, runs the same multi-GPU step (exchange included)
+    # and reads this rank's rows of y back; CUDA events on the stream, max over ranks
+    e2e_ms_local, h2d_local, d2h_local = 0.0, 0, 0
+    if not args.no_extras:
+        b0, b1 = int(b[rank]), int(b[rank + 1])
+        srcs = [(M.row_offsets, M.row_offsets.cpu().pin_memory()), (M.col_idx, M.col_idx.cpu().pin_memory()),
+                (M.values, M.values.cpu().pin_memory()), (x, x.cpu().pin_memory())]
+        h_y = torch.empty(b1 - b0, pin_memory=True)
+        h2d_local = sum(h.numel() * h.element_size() for _, h in srcs)
+        d2h_local = h_y.numel() * 4
+
+        def e2e_step():
+            for d_t, h_t in srcs:
+                d_t.copy_(h_t, non_blocking=True)
+            step()
+            h_y.copy_(y[b0:b1], non_blocking=True)
+
+        e2e_step()
+        e2e_ms_local = timed(e2e_step, args.e2e_steps)
+    t = torch.tensor([ms_local, spmv_ms_local, e2e_ms_local, float(h2d_local), float(d2h_local)],
+                     dtype=torch.float64, device=dev)
+    tmax = t.clone()
+    dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    ms, spmv_ms, e2e_ms = float(tmax[0]), float(tmax[1]), float(tmax[2])
+    h2d_total, d2h_total = int(t[3]), int(t[4])
     if rank == 0:
         rec = {
             "metric": "SpMV GNZ/s", "value": round(nnz / (ms * 1e-3) / 1e9, 3), "unit": "GNZ/s", "n_gpus": world,
@@ -450,8 +480,22 @@ def run_multi(args, cfg):
             "no_plan": no_plan,
             "gpu_launches": int(launches),
             "spmv_only": {"value": round(nnz / (spmv_ms * 1e-3) / 1e9, 3), "unit": "GNZ/s", "ms": round(spmv_ms, 5)},
-            "e2e": None,
+            "e2e": None if args.no_extras else {
+                "value": round(nnz / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GNZ/s", "h2d_bytes_per_step": h2d_total,
+                "d2h_bytes_per_step": d2h_total, "steps": args.e2e_steps,
+                "api": "per rank: pinned H2D of the shard CSR + x, the same multi-GPU step, D2H of the rank's y rows; "
+                       "CUDA events, max over ranks; bytes summed over ranks"},
         }
+        # roofline of rank 0's tile kernel on its shard (phase times: CUDA events on the launch stream)
+        ph = [M.phase_times(x, y[int(b[0]):int(b[1])], args.schedule) for _ in range(10)]
+        main_ms = float(np.mean([p_[1] for p_ in ph]))
+        alg = compulsory_bytes(M.rows, cols, M.nnz)
+        peak, peak_src = peak_hbm()
+        achieved = alg / (main_ms * 1e-3) / 1e9
+        rec["roofline"] = {"bound": "hbm", "kernel": M.kernel_name(args.schedule), "achieved": round(achieved, 1),
+                           "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                           "algorithmic_bytes": alg, "peak_source": peak_src,
+                           "kernel_ms_from": "rank 0 shard: mean of 10 lb_spmv_phase_times calls"}
         if sampler:
             rec["clocks"] = sampler.summary()
         print(json.dumps(rec))
