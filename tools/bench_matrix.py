@@ -41,11 +41,18 @@ for cfg in CFGS:
             n = 200
         ms_step = timeit(lambda: M.spmv(x, y, sched, repartition=True), n)
         ms_cached = timeit(lambda: M.spmv(x, y, sched), n)
+        # the same step captured once in a CUDA graph and replayed (no per-call host launch cost)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            M.spmv(x, y, sched, repartition=True)
+        ms_graph = timeit(g.replay, n)
+        del g
         print(json.dumps({"config": cfg, "rows": A.rows, "nnz": A.nnz, "schedule": sched, "plan": plan,
                           "kernel": M.kernel_name(sched), "L": M.items_per_tile if sched == "merge_path" else None,
                           "ms_step": round(ms_step, 4), "GNZ/s_step": round(A.nnz / ms_step / 1e6, 2),
                           "ms_cached_partition": round(ms_cached, 4),
                           "GNZ/s_cached": round(A.nnz / ms_cached / 1e6, 2),
+                          "ms_graph": round(ms_graph, 4), "GNZ/s_graph": round(A.nnz / ms_graph / 1e6, 2),
                           "alg_GB/s_cached": round(alg / ms_cached / 1e6, 1)}), flush=True)
     del M, A, x, y
     torch.cuda.empty_cache()
