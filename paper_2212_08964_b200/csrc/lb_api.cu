@@ -1107,11 +1107,12 @@ lb_status_t sssp_impl(lb_csr_s* A, int64_t source, lb_schedule_t sched, float* d
 
 constexpr int kSpmmW = 8, kSpmmMinB = 2, kSpmmL = 1016;
 
-template <int P>
+// P columns per panel; E nonzeros per lane per round (P = 8 panels use E = 2 to fit the registers)
+template <int P, int E = 4>
 lb_status_t spmm_panel(lb_csr_s* A, const float* X, int64_t ldx, float* Y, int64_t ldy, stream_t s) {
-  auto k = lbk::merge_spmm_kernel<kSpmmW, P, kSpmmMinB>;
-  static int blocks_cache[64][2] = {{0}};
-  int& blocks = blocks_cache[A->device][P == 4];
+  auto k = lbk::merge_spmm_kernel<kSpmmW, P, kSpmmMinB, E>;
+  static int blocks_cache[64][3] = {{0}};
+  int& blocks = blocks_cache[A->device][P == 8 ? 2 : P == 4];
   if (blocks == 0) {
     cudaFuncAttributes fa;
     LB_CUDA(cudaFuncGetAttributes(&fa, k));
@@ -1123,7 +1124,8 @@ lb_status_t spmm_panel(lb_csr_s* A, const float* X, int64_t ldx, float* Y, int64
     blocks = std::max(1, blocks);
   }
   const int T = (int)num_tiles(A->rows, A->nnz, kSpmmL);
-  const int warps_max = std::min(A->dev->sm_count * blocks * kSpmmW, kMaxCtas);
+  // carry_val holds 4 * kMaxCtas floats: P values per warp
+  const int warps_max = std::min(A->dev->sm_count * blocks * kSpmmW, 4 * kMaxCtas / P);
   const int tpw = (T + warps_max - 1) / warps_max;
   const int warps = (T + tpw - 1) / tpw;
   const int grid = (warps + kSpmmW - 1) / kSpmmW;
@@ -1150,9 +1152,15 @@ lb_status_t spmm_impl(lb_csr_s* A, int64_t n, const float* X, int64_t ldx, float
     A->coords_kind = 0;
   }
   for (int64_t c0 = 0; c0 < n;) {
+    // 8-column panels gather one 32-byte sector per nonzero (X rows 32-byte aligned)
+    const bool oct = n - c0 >= 8 && ldx % 8 == 0 && ldy % 4 == 0 &&
+                     reinterpret_cast<uintptr_t>(X + c0) % 32 == 0 && reinterpret_cast<uintptr_t>(Y + c0) % 16 == 0;
     const bool quad = n - c0 >= 4 && ldx % 4 == 0 && ldy % 4 == 0 &&
                       reinterpret_cast<uintptr_t>(X + c0) % 16 == 0 && reinterpret_cast<uintptr_t>(Y + c0) % 16 == 0;
-    if (quad) {
+    if (oct) {
+      if ((st = spmm_panel<8, 2>(A, X + c0, ldx, Y + c0, ldy, s)) != LB_OK) return st;
+      c0 += 8;
+    } else if (quad) {
       if ((st = spmm_panel<4>(A, X + c0, ldx, Y + c0, ldy, s)) != LB_OK) return st;
       c0 += 4;
     } else {

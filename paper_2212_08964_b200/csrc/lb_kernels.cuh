@@ -1875,11 +1875,20 @@ template <>
 struct PVec<4> {
   float v[4];
 };
+template <>
+struct PVec<8> {
+  float v[8];
+};
 
 template <int P>
 __device__ __forceinline__ void spmm_gather(const SpmmArgs& a, int c, PVec<P>& out) {
   const float* src = a.X + (int64_t)c * a.ldx;
-  if (P == 4) {
+  if (P == 8) {  // one 32-byte sector per nonzero: a single 256-bit gather
+    asm("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+        : "=f"(out.v[0]), "=f"(out.v[1]), "=f"(out.v[2]), "=f"(out.v[3]), "=f"(out.v[4]), "=f"(out.v[5]),
+          "=f"(out.v[6]), "=f"(out.v[7])
+        : "l"(src));
+  } else if (P == 4) {
     const float4 t = __ldg(reinterpret_cast<const float4*>(src));
     out.v[0] = t.x; out.v[1] = t.y; out.v[2] = t.z; out.v[3] = t.w;
   } else {
@@ -1890,25 +1899,42 @@ __device__ __forceinline__ void spmm_gather(const SpmmArgs& a, int c, PVec<P>& o
 template <int P>
 __device__ __forceinline__ void spmm_store(const SpmmArgs& a, int row, const float (&v)[P]) {
   float* dst = a.Y + (int64_t)row * a.ldy;
-  if (P == 4) __stcs(reinterpret_cast<float4*>(dst), make_float4(v[0], v[1], v[2], v[3]));
-  else __stcs(dst, v[0]);
+  if (P == 8) {
+    __stcs(reinterpret_cast<float4*>(dst), make_float4(v[0], v[1], v[2], v[3]));
+    __stcs(reinterpret_cast<float4*>(dst) + 1, make_float4(v[4], v[5], v[6], v[7]));
+  } else if (P == 4) {
+    __stcs(reinterpret_cast<float4*>(dst), make_float4(v[0], v[1], v[2], v[3]));
+  } else {
+    __stcs(dst, v[0]);
+  }
 }
 
+// E consecutive nonzeros per lane per round (a round = 32 E nonzeros)
+template <int E>
 struct SpmmRound {
-  int col[4];
-  float val[4];
+  int col[E];
+  float val[E];
 };
 
-__device__ __forceinline__ void spmm_load(const SpmmArgs& a, int4 c, int k, int lane, SpmmRound& d) {
-  const int g = (c.y & ~7) + 128 * k + 4 * lane;
-  if (a.vec && g < c.w && g + 4 <= a.nnz) {
-    const int4 ci = ld_cs_v4(a.col + g);
-    const float4 vi = ld_cs_v4(a.val + g);
-    d.col[0] = ci.x; d.col[1] = ci.y; d.col[2] = ci.z; d.col[3] = ci.w;
-    d.val[0] = vi.x; d.val[1] = vi.y; d.val[2] = vi.z; d.val[3] = vi.w;
+template <int E>
+__device__ __forceinline__ void spmm_load(const SpmmArgs& a, int4 c, int k, int lane, SpmmRound<E>& d) {
+  const int g = (c.y & ~7) + 32 * E * k + E * lane;
+  if (a.vec && g < c.w && g + E <= a.nnz) {
+    if constexpr (E == 4) {
+      const int4 ci = ld_cs_v4(a.col + g);
+      const float4 vi = ld_cs_v4(a.val + g);
+      d.col[0] = ci.x; d.col[1] = ci.y; d.col[2] = ci.z; d.col[3] = ci.w;
+      d.val[0] = vi.x; d.val[1] = vi.y; d.val[2] = vi.z; d.val[3] = vi.w;
+    } else {
+      static_assert(E == 2, "E: 2 or 4 nonzeros per lane");
+      const int2 ci = __ldcs(reinterpret_cast<const int2*>(a.col + g));
+      const float2 vi = __ldcs(reinterpret_cast<const float2*>(a.val + g));
+      d.col[0] = ci.x; d.col[1] = ci.y;
+      d.val[0] = vi.x; d.val[1] = vi.y;
+    }
   } else {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
+    for (int e = 0; e < E; ++e) {
       const bool ok = g + e < c.w;
       d.col[e] = ok ? ld_cs(a.col + g + e) : 0;
       d.val[e] = ok ? ld_cs(a.val + g + e) : 0.f;
@@ -1916,12 +1942,12 @@ __device__ __forceinline__ void spmm_load(const SpmmArgs& a, int4 c, int k, int 
   }
 }
 
-template <int P>
-__device__ __forceinline__ void spmm_gather_round(const SpmmArgs& a, int4 c, int k, int lane, SpmmRound& d,
-                                                  PVec<P> (&xv)[4]) {
-  const int q0 = 128 * k + 4 * lane, lo = c.y & 7, hi = c.w - (c.y & ~7);
+template <int P, int E>
+__device__ __forceinline__ void spmm_gather_round(const SpmmArgs& a, int4 c, int k, int lane, SpmmRound<E>& d,
+                                                  PVec<P> (&xv)[E]) {
+  const int q0 = 32 * E * k + E * lane, lo = c.y & 7, hi = c.w - (c.y & ~7);
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
+  for (int e = 0; e < E; ++e) {
     const bool ok = q0 + e >= lo && q0 + e < hi;
     if (ok) spmm_gather<P>(a, d.col[e], xv[e]);
     else {
@@ -1932,9 +1958,9 @@ __device__ __forceinline__ void spmm_gather_round(const SpmmArgs& a, int4 c, int
   }
 }
 
-template <int W, int P, int MINB>
+template <int W, int P, int MINB, int E = 4>
 __global__ void __launch_bounds__(W * 32, MINB) merge_spmm_kernel(SpmmArgs a) {
-  constexpr int kCap = 1024, R = 8;  // tile positions, rounds of 128 per tile (L = 1016)
+  constexpr int kCap = 1024, R = kCap / (32 * E);  // tile positions, rounds of 32 E per tile (L = 1016)
   constexpr int K = 2;
   __shared__ __align__(16) unsigned short s_tail[W][kCap];
   __shared__ int s_last;
@@ -1995,21 +2021,21 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_spmm_kernel(SpmmArgs a) {
     bool r0e = row_pass(cT);
     if (t_begin + 1 < t_end) stream_prefetch_offsets<4, K>(pa, cT1, lane, olo, ohi);
     __syncwarp();
-    SpmmRound d0, d1, d2;
-    PVec<P> x0[4], x1[4];
-    spmm_load(a, cT, 0, lane, d0);
-    if (1 < nsteps) spmm_load(a, cT, 1, lane, d1);
-    spmm_gather_round<P>(a, cT, 0, lane, d0, x0);
+    SpmmRound<E> d0, d1, d2;
+    PVec<P> x0[E], x1[E];
+    spmm_load<E>(a, cT, 0, lane, d0);
+    if (1 < nsteps) spmm_load<E>(a, R > 1 ? cT : cT1, R > 1 ? 1 : 0, lane, d1);
+    spmm_gather_round<P, E>(a, cT, 0, lane, d0, x0);
     int t = t_begin, k = 0;
     for (int st = 0; st < nsteps; ++st) {
       if (st + 1 < nsteps) {
         const bool same = k + 1 < R;
-        spmm_gather_round<P>(a, same ? cT : cT1, same ? k + 1 : k + 1 - R, lane, d1, x1);
+        spmm_gather_round<P, E>(a, same ? cT : cT1, same ? k + 1 : k + 1 - R, lane, d1, x1);
       }
       if (st + 2 < nsteps) {
         const int k2 = k + 2;
         const bool same = k2 < R;
-        spmm_load(a, same ? cT : cT1, same ? k2 : k2 - R, lane, d2);
+        spmm_load<E>(a, same ? cT : cT1, same ? k2 : k2 - R, lane, d2);
       }
       const int i0 = cT.x;
       if (k == 0 && r0e) {
@@ -2017,14 +2043,21 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_spmm_kernel(SpmmArgs a) {
 #pragma unroll
         for (int j = 0; j < P; ++j) rc[j] = 0.f;
       }
-      const uint2 tq = *reinterpret_cast<const uint2*>(&tail[128 * k + 4 * lane]);
-      const unsigned rid[4] = {tq.x & 0xFFFFu, tq.x >> 16, tq.y & 0xFFFFu, tq.y >> 16};
+      unsigned rid[E];
+      uint2 tq = make_uint2(0u, 0u);
+      if constexpr (E == 4) {
+        tq = *reinterpret_cast<const uint2*>(&tail[128 * k + 4 * lane]);
+        rid[0] = tq.x & 0xFFFFu; rid[1] = tq.x >> 16; rid[2] = tq.y & 0xFFFFu; rid[3] = tq.y >> 16;
+      } else {
+        tq.x = *reinterpret_cast<const unsigned*>(&tail[64 * k + 2 * lane]);
+        rid[0] = tq.x & 0xFFFFu; rid[1] = tq.x >> 16;
+      }
       float run[P], first_val[P];
 #pragma unroll
       for (int j = 0; j < P; ++j) { run[j] = 0.f; first_val[j] = 0.f; }
       int first_r = -1;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < E; ++e) {
 #pragma unroll
         for (int j = 0; j < P; ++j) run[j] = fmaf(d0.val[e], x0[e].v[j], run[j]);
         if (rid[e]) {
@@ -2070,11 +2103,14 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_spmm_kernel(SpmmArgs a) {
         for (int j = 0; j < P; ++j) yv[j] = (lane == 0 ? rc[j] : (lf ? lval[j] : rc[j] + lval[j])) + first_val[j];
         spmm_store<P>(a, i0 + first_r, yv);
       }
-      if (tq.x | tq.y) *reinterpret_cast<uint2*>(&tail[128 * k + 4 * lane]) = make_uint2(0u, 0u);
+      if (tq.x | tq.y) {
+        if constexpr (E == 4) *reinterpret_cast<uint2*>(&tail[128 * k + 4 * lane]) = make_uint2(0u, 0u);
+        else *reinterpret_cast<unsigned*>(&tail[64 * k + 2 * lane]) = 0u;
+      }
 #pragma unroll
       for (int j = 0; j < P; ++j) rc[j] = agg_f ? agg_v[j] : rc[j] + agg_v[j];
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < E; ++e) {
         d0.val[e] = d1.val[e];
         x0[e] = x1[e];
         d1.col[e] = d2.col[e];

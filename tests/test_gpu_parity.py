@@ -482,6 +482,13 @@ def test_spmm_strided_and_edge_cases():
     Y_ref, S_ref = oracle.spmm(A.row_offsets, A.col_idx, A.values, X.cpu().contiguous())
     M = lb.CsrMatrix.from_csr(A)
     check_Y(M.spmm(X), Y_ref, S_ref, True, "strided")
+    # ldx = 16 with panels starting at columns 0 and 8 (8-column panels) and at 4 (misaligned for 8:
+    # a 4-column panel first), plus a 13-column view: 8 + 4 + 1
+    X16 = lbgen.make_x(A.cols * 16, "int", 4).reshape(A.cols, 16).cuda()
+    for lo, hi in ((0, 16), (4, 16), (0, 13), (8, 16)):
+        Xv = X16[:, lo:hi]
+        Y_ref, S_ref = oracle.spmm(A.row_offsets, A.col_idx, A.values, Xv.cpu().contiguous())
+        check_Y(M.spmm(Xv), Y_ref, S_ref, True, f"ldx16[{lo}:{hi}]")
     for nm, B in {"giant": _csr([0, 50_001], 1), "no_nnz": _csr([0] * 2001, 3),
                   "golden": _csr([0, 1, 3, 3, 6], 1)}.items():
         X = torch.ones(B.cols, 4)
@@ -496,16 +503,17 @@ def test_spmm_strided_and_edge_cases():
     check_Y(Y, Y_ref, S_ref, False, "float n=4")
 
 
-@pytest.mark.parametrize("cfg", ["c3", "c4"])
-def test_spmm_full_size(cfg):
+@pytest.mark.parametrize("cfg,n", [("c3", 4), ("c4", 4), ("c3", 8)])
+def test_spmm_full_size(cfg, n):
+    """Full-size SpMM: 4-column panels, and an 8-column panel (one 256-bit gather per nonzero)."""
     torch.cuda.empty_cache()
     A = lbgen.make_config(cfg, "int", device="cuda")
-    X = lbgen.make_x(A.cols * 4, "int", 77, device="cuda").reshape(A.cols, 4)
+    X = lbgen.make_x(A.cols * n, "int", 77, device="cuda").reshape(A.cols, n)
     M = lb.CsrMatrix.from_csr(A)
     Y = M.spmm(X)
     torch.cuda.synchronize()
     Yh = Y.cpu()
-    for j in range(4):   # column by column through the oracle SpMV (exact in integer mode)
+    for j in range(n):   # column by column through the oracle SpMV (exact in integer mode)
         y_ref, s_ref = oracle.spmv(A.row_offsets.cpu(), A.col_idx.cpu(), A.values.cpu(), X[:, j].cpu(), threads=True)
         check_y(Yh[:, j], y_ref, s_ref, True, f"{cfg} col {j}")
     del M, A, X, Y
