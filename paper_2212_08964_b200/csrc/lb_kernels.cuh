@@ -1668,11 +1668,26 @@ __global__ void plan_remap_kernel(int64_t nnz, int cols, int n_hot, const int* _
 // takes 32 frontier vertices and strides their edge pool, Alg.2) or merge-path (frontier vertices +
 // edges split evenly into per-thread diagonal ranges, each found by the 2-D search, Alg.3).
 
+// Relax edge (u -> v) with candidate distance nd = dist[u] + w.  A plain read of dist[v] first
+// skips the atomic when nd cannot improve it (distances only decrease, so a stale read is never
+// smaller than the current value); the vertices pushed to the next frontier are counted with one
+// atomicAdd per group of lanes that push together (warp-aggregated).
 __device__ __forceinline__ void sssp_relax(int v, float nd, float* __restrict__ dist, int* __restrict__ stamp,
                                            int round, int* __restrict__ q_out, int* __restrict__ n_out) {
-  const int old = atomicMin(reinterpret_cast<int*>(dist) + v, __float_as_int(nd));
-  if (__float_as_int(nd) < old) {
-    if (atomicExch(stamp + v, round) != round) q_out[atomicAdd(n_out, 1)] = v;
+  bool push = false;
+  if (__float_as_int(nd) < __ldcg(reinterpret_cast<const int*>(dist) + v)) {
+    const int old = atomicMin(reinterpret_cast<int*>(dist) + v, __float_as_int(nd));
+    push = __float_as_int(nd) < old && atomicExch(stamp + v, round) != round;
+  }
+  const unsigned active = __activemask();
+  const unsigned m = __ballot_sync(active, push);
+  if (push) {
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(m) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(n_out, __popc(m));
+    base = __shfl_sync(m, base, leader);
+    q_out[base + __popc(m & ((1u << lane) - 1u))] = v;
   }
 }
 
@@ -1843,7 +1858,7 @@ __global__ void __launch_bounds__(256) frontier_deg_scan_kernel(int F, const int
 }
 
 // ----------------------------------------------------------------------------- SpMM (NEXT-2)
-// Y = A X for a panel of P (1 or 4) columns of a row-major X (Listing 4: "a simple loop
+// Y = A X for a panel of P (1, 4 or 8) columns of a row-major X (Listing 4: "a simple loop
 // wrapped around SpMV"), on the same merge-path tiles as SpMV (L = 1016, lb_partition's output is
 // reused).  Warp-streamed like merge_stream_kernel, with 4 nonzeros per lane per round (128 per
 // warp-round, 8 rounds per tile) and one P-wide gather X[col, c0 .. c0+P) per nonzero: with P = 4
