@@ -19,7 +19,8 @@
  *  - Errors: a status code is returned; no exception crosses the ABI.  lb_last_error()
  *    returns a thread-local message for the last failing call on this thread.
  *  - Index widths: int32 row offsets and column indices, fp32 values, x and y (P:963-969,
- *    Listing 3).  Sizes are int64; rows + nnz must be < 2^31 (reading R13).
+ *    Listing 3).  Sizes are int64; rows + nnz must be <= 2^31 - 2^16 - 1 (int32 indices with headroom
+ *    for tile overshoot; reading R13).
  *  - y is OVERWRITTEN (y = A x, not y += A x; "y[row] = sum", Alg.3).
  *  - Empty rows produce y = +0 (P:982 with the zero-initialised sum); rows == 0 is a no-op.
  *  - There is no CPU fallback: every compute call runs CUDA kernels of this library and
@@ -37,7 +38,7 @@ extern "C" {
 
 typedef enum {
   LB_OK = 0,
-  LB_ERR_INVALID_ARG = 1,  /* null pointer with non-zero size, negative size, rows+nnz >= 2^31,
+  LB_ERR_INVALID_ARG = 1,  /* null pointer with non-zero size, negative size, rows+nnz > 2^31-2^16-1,
                               unknown schedule, unsupported items_per_tile, x aliasing y, ... */
   LB_ERR_INVALID_CSR = 2,  /* validation failed: off[0] != 0, off not non-decreasing,
                               off[rows] != nnz, or a column index outside [0, cols) */
@@ -107,7 +108,8 @@ typedef struct lb_comm_s* lb_comm_t; /* opaque multi-GPU communicator (wraps an 
 /*
  * lb_csr_create -- borrow a CSR matrix (P:149 [Sec. CSR]: row offsets = prefix sum of row
  * lengths, column indices and values in row-major order).
- *  rows, cols, nnz     matrix shape and number of stored entries (>= 0; rows + nnz < 2^31).
+ *  rows, cols, nnz     matrix shape and number of stored entries (>= 0; rows + nnz <= 2^31 - 2^16 - 1,
+ *                      cols < 2^31 - 1).
  *  d_row_offsets       int32[rows+1], d_col_idx int32[nnz], d_values fp32[nnz] (device).
  *  validate            1: run the validation kernel (off[0] = 0, off non-decreasing,
  *                      off[rows] = nnz, 0 <= col < cols) and synchronise `stream` once to read

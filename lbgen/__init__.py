@@ -272,6 +272,39 @@ def uniform_rows(scale: int, per_row: int, seed: int, vmode: str, device="cpu") 
     return skewed(rows, 0, 0, rows * per_row, seed, vmode, device)
 
 
+MAX_MERGE_ITEMS = (1 << 31) - (1 << 16) - 1  # largest rows + nnz the C ABI accepts (include/lb.h)
+
+
+def max_size(seed: int, vmode: str, device="cpu", cols: int = 1 << 20, giant: int = 200_000) -> Csr:
+    """The largest merge-path problem the API accepts: rows + nnz = MAX_MERGE_ITEMS exactly, nnz = 2^30.
+    Ragged rows repeating (2, 0, 1) nonzeros (a third of the rows empty), row 5 a giant row of
+    1 + `giant` nonzeros paid for by emptying `giant` / 2 of the 2-rows after it, and the last row taking
+    the remainder that makes nnz exact.  Columns: counter hash, uniform over `cols`."""
+    nnz = 1 << 30
+    rows = MAX_MERGE_ITEMS - nnz
+    r = _arange(rows, device)
+    lengths = torch.where(r % 3 == 0, 2, torch.where(r % 3 == 1, 0, 1))
+    del r
+    lengths[5] += giant
+    lengths[6:6 + 3 * (giant // 2):3] = 0  # rows 6, 9, ... (each had 2)
+    lengths[-1] = 0
+    rest = nnz - int(lengths.sum())
+    assert rest >= 0
+    lengths[-1] = rest
+    off64 = _offsets_from_lengths(lengths)
+    del lengths
+    assert int(off64[-1]) == nnz
+    col = torch.empty(nnz, dtype=torch.int32, device=device)
+    cbits = (cols - 1).bit_length()
+    assert cols == 1 << cbits
+    chunk = 1 << 26
+    for s in range(0, nnz, chunk):
+        e = min(nnz, s + chunk)
+        col[s:e] = _srl(hash64(seed, _arange(e - s, device) + s), 64 - cbits).to(torch.int32)
+    vals = assign_values(nnz, vmode, seed, device)
+    return Csr(rows, cols, off64.to(torch.int32), col, vals, "max_size")
+
+
 def make_config(name: str, vmode: str = "float", device="cpu") -> Csr:
     c = dict(CONFIGS[name])
     kind = c.pop("kind")

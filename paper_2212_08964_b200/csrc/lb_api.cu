@@ -48,6 +48,9 @@ lb_status_t fail(lb_status_t st, const char* fmt, ...) {
   } while (0)
 
 constexpr int kNT = 256;
+// rows + nnz limit: int32 indices with 2^16 of headroom for the rounds / tiles that overshoot the last
+// nonzero inside the kernels' int32 position arithmetic
+constexpr int64_t kMaxMergeItems = (1ll << 31) - (1ll << 16) - 1;
 constexpr int kMaxCtas = 8192;      // carry slots per handle (>= SMs x resident CTAs)
 constexpr int kMinTile = 504;       // smallest supported L: sizes the partition cache
 
@@ -312,8 +315,8 @@ int auto_tile_length(int64_t rows, int64_t nnz) { return nnz < 8 * rows ? 2040 :
 lb_status_t check_shape(int64_t rows, int64_t cols, int64_t nnz) {
   if (rows < 0 || cols < 0 || nnz < 0) return fail(LB_ERR_INVALID_ARG, "negative size (rows=%lld cols=%lld nnz=%lld)",
                                                    (long long)rows, (long long)cols, (long long)nnz);
-  if (rows + nnz >= (int64_t)INT_MAX || cols >= (int64_t)INT_MAX)
-    return fail(LB_ERR_INVALID_ARG, "rows + nnz and cols must be < 2^31 (int32 indices)");
+  if (rows + nnz > kMaxMergeItems || cols >= (int64_t)INT_MAX)
+    return fail(LB_ERR_INVALID_ARG, "rows + nnz must be <= 2^31 - 2^16 - 1 and cols < 2^31 - 1 (int32 indices)");
   if (nnz > 0 && cols == 0) return fail(LB_ERR_INVALID_ARG, "nnz > 0 with cols == 0");
   return LB_OK;
 }

@@ -67,3 +67,16 @@ def test_compute_without_gpu_fails_loudly():
     st = L.lb_csr_create(1, 1, 0, ctypes.c_void_p(16), None, None, 0, None, ctypes.byref(h))
     assert st == lb.lb.LB_ERR_CUDA
     assert lb.last_error()
+
+
+def test_shape_limits_checked_before_any_access():
+    """Size errors come back as LB_ERR_INVALID_ARG before the library touches the arrays or the device:
+    rows + nnz above 2^31 - 2^16 - 1 (lbgen.MAX_MERGE_ITEMS), cols >= 2^31 - 1, negative sizes."""
+    L = lb.lib()
+    fake = ctypes.c_void_p(256)  # never dereferenced
+    cases = [(lbgen.MAX_MERGE_ITEMS - (1 << 30) + 1, 1 << 20, 1 << 30), (1, (1 << 31) - 1, 1), (-1, 1, 0), (1, 1, -2)]
+    for rows, cols, nnz in cases:
+        h = ctypes.c_void_p()
+        st = L.lb_csr_create(rows, cols, nnz, fake, fake, fake, 0, None, ctypes.byref(h))
+        assert st == lb.lb.LB_ERR_INVALID_ARG and not h, (rows, cols, nnz)
+        assert "2^31" in lb.last_error() or "negative" in lb.last_error()

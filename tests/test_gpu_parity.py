@@ -10,6 +10,8 @@ Sizes span several tiles and ragged tails; full BASELINE.json sizes are covered 
 test_full_size_configs (partition bit-exact on every tile, y on every row for C1-C4 and on
 sampled rows for C5).
 """
+import ctypes
+
 import numpy as np
 import pytest
 import torch
@@ -575,3 +577,36 @@ def test_cuda_graph_capture_and_replay(sched):
         torch.cuda.synchronize()
         y_ref, s_ref = ref(A, xi)
         check_y(y, y_ref, s_ref, True, f"graph/{sched}")
+
+
+# ---------------------------------------------------------------- the int32 / int64 limits
+
+def test_maximum_size_merge_items():
+    """The largest problem the API accepts, rows + nnz = 2^31 - 2^16 - 1 (nnz = 2^30, ragged rows, a third
+    of them empty, a 200,001-nonzero row and a ~65K-nonzero last row): the partition is bit-exact on every
+    tile (brute-force oracle over all merge items) and y is bit-exact (integer mode) on sampled rows for the
+    merge-path, nonzero-split and binning schedules; one more merge item is rejected."""
+    torch.cuda.empty_cache()
+    A = lbgen.max_size(31, "int", device="cuda")
+    assert A.rows + A.nnz == lbgen.MAX_MERGE_ITEMS
+    h = ctypes.c_void_p()  # shape checks come before any access to the arrays
+    st = lb.lib().lb_csr_create(A.rows + 1, A.cols, A.nnz, A.row_offsets.data_ptr(), A.col_idx.data_ptr(),
+                                A.values.data_ptr(), 0, None, ctypes.byref(h))
+    assert st == lb.lb.LB_ERR_INVALID_ARG and not h
+    x = lbgen.make_x(A.cols, "int", 8, device="cuda")
+    M = lb.CsrMatrix.from_csr(A, device="cuda", validate=True)
+    coords = M.partition().cpu().numpy()
+    assert coords[-1].tolist() == [A.rows, A.nnz]
+    assert np.array_equal(coords, oracle.partition(A.row_offsets.cpu(), M.items_per_tile)), "partition"
+    sel = _sample_rows(A, coords, 20_000, 3)
+    so, sc, sv = _packed(A, sel)
+    y_ref, s_ref = oracle.spmv_packed(so, sc, sv, x.cpu())
+    sel_d = torch.as_tensor(sel, device="cuda")
+    for sched in ("merge_path", "nonzero_split", "binning"):
+        y = torch.full((A.rows,), float("nan"), device="cuda")
+        M.spmv(x, y, sched, repartition=True)
+        torch.cuda.synchronize()
+        check_y(y[sel_d], y_ref, s_ref, True, f"max_size/{sched}")
+        del y
+    del M, A, x
+    torch.cuda.empty_cache()
