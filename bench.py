@@ -121,7 +121,7 @@ class ClockSampler:
             if len(f) < 9:
                 continue
             try:
-                rows.append(dict(sm=float(f[1]), smax=float(f[2]), util=float(f[4]),
+                rows.append(dict(sm=float(f[1]), smax=float(f[2]), power=float(f[3]), util=float(f[4]),
                                  hw=f[5], hwt=f[6], swt=f[7], pcap=f[8]))
             except ValueError:
                 continue
@@ -132,7 +132,8 @@ class ClockSampler:
                  "pcap": "sw_power_cap"}
         reasons = sorted({n for r in load for k, n in names.items() if r[k].lower().startswith("active")})
         return {"sm_mhz": statistics.median(r["sm"] for r in load), "sm_max_mhz": max(r["smax"] for r in load),
-                "reasons": reasons, "samples": len(load)}
+                "reasons": reasons, "samples": len(load), "power_w_median": statistics.median(r["power"] for r in load),
+                "power_w_max": max(r["power"] for r in load)}
 
 
 def dist_env():
