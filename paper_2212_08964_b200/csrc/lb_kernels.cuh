@@ -1149,9 +1149,9 @@ __device__ __forceinline__ void stream_prefetch_offsets(const PipeArgs& a, int4 
   }
 }
 
-// y stores of the warp-streamed kernel.  With PEERS the value also goes to every other rank's copy of
-// y (NVLink peer stores: the all-gather of lb_spmv_multi fused into the epilogue);
-// `peers` = false for a partial value (a row the fix-up completes), which stays local.
+// y stores of the warp-streamed kernel.  With PEERS (the fix-up of the fused multi-GPU epilogue,
+// DESIGN.md 7b) the value also goes to every other rank's copy of y over NVLink; `peers` = false for a
+// partial value, which stays local.
 template <bool PEERS>
 __device__ __forceinline__ void put_y(const PipeArgs& a, int idx, float v, bool peers = true) {
   __stcs(a.y + idx, v);
@@ -1161,20 +1161,11 @@ __device__ __forceinline__ void put_y(const PipeArgs& a, int idx, float v, bool 
       if (p < a.npeers) __stcg(a.peer_y[p] + idx, v);
   }
 }
-template <bool PEERS>
-__device__ __forceinline__ void put_y_if(const PipeArgs& a, float* yt, unsigned rid, int yt_off, float v, bool pred) {
-  st_cs_if(yt + rid, v, pred);
-  if (PEERS) {
-#pragma unroll
-    for (int p = 0; p < kMaxPeers; ++p)
-      if (p < a.npeers && pred) __stcg(a.peer_y[p] + yt_off + (int)rid, v);
-  }
-}
 
 // Row pass of tile c into tail[]: tail[q] = r + 1 when local nonzero q ends row r (r >= 0);
 // rows r > 0 with no nonzero in the tile get y = 0; returns (warp-uniform) whether row 0 has no
 // nonzero in the tile (its value is then the carry entering the tile).
-template <int R, int K, typename TailT, bool PEERS = false>
+template <int R, int K, typename TailT>
 __device__ __forceinline__ bool stream_row_pass(const PipeArgs& a, int4 c, int lane, const int (&lo_)[K],
                                                 const int (&hi_)[K], TailT* tail) {
   const int i0 = c.x, nrows = c.z - c.x, jA = c.y & ~7, lo = c.y - jA;
@@ -1195,7 +1186,7 @@ __device__ __forceinline__ bool stream_row_pass(const PipeArgs& a, int4 c, int l
       const int e = oe - jA;
       const int s = r == 0 ? lo : ob - jA;
       if (e > s) tail[e - 1] = (TailT)(r + 1);
-      else if (r > 0) put_y<PEERS>(a, i0 + r, 0.f);
+      else if (r > 0) put_y<false>(a, i0 + r, 0.f);
       else row0_empty = true;
     }
   }
@@ -1220,16 +1211,32 @@ __device__ __forceinline__ void tail_clear8(unsigned* p) {
   *reinterpret_cast<uint4*>(p + 4) = make_uint4(0u, 0u, 0u, 0u);
 }
 
+// Fused multi-GPU epilogue (PEERS): when a tile is done, its final rows [i0, i1) -- every row that ends
+// in the tile, written to the local y by this warp (the row pass, the rounds) -- are copied to every
+// other rank's y with coalesced stores over NVLink.  The warp's first row is excluded when it started
+// before the warp's run (`open_row`, partial: the fix-up completes it and sends it).  One coalesced
+// pass per tile instead of a peer store per row end keeps the epilogue off the rounds' critical path
+// (measured: a software-pipelined variant of this copy was no faster).
+__device__ __forceinline__ void stream_peer_copy(const PipeArgs& a, int4 c, int open_row, int lane) {
+  const int r0 = c.x == open_row ? c.x + 1 : c.x;
+  for (int r = r0 + lane; r < c.z; r += 32) {
+    const float v = __ldcg(a.y + r);  // this warp's own stores, ordered by the __syncwarp before the call
+#pragma unroll
+    for (int p = 0; p < kMaxPeers; ++p)
+      if (p < a.npeers) __stcg(a.peer_y[p] + r, v);
+  }
+}
+
 // Reduce one round (256 nonzeros) of tile c: products val*x summed per lane, rows that end after
 // the lane's first row end are stored directly, the ballot-based segmented scan gives each lane's
 // first row its carry-in, and `rc` (warp-uniform) carries the open row's partial to the next round.
-template <bool PEERS, typename TailT>
-__device__ __forceinline__ void stream_reduce_round(const PipeArgs& a, int4 cT, int k, int lane, bool r0e, int open_row,
+template <typename TailT>
+__device__ __forceinline__ void stream_reduce_round(const PipeArgs& a, int4 cT, int k, int lane, bool r0e,
                                                     float (&val)[8], const float (&xc)[8], TailT* tail, float& rc) {
   // (b) the row open at the tile start has no nonzero here: it ends now with the carry
   const int i0 = cT.x;
   if (k == 0 && r0e) {
-    if (lane == 0) put_y<PEERS>(a, i0, rc, i0 != open_row);
+    if (lane == 0) put_y<false>(a, i0, rc);
     rc = 0.f;
   }
   // (c) positions outside the tile's nonzero range [lo, hi) add exactly zero (warp-uniform test)
@@ -1259,7 +1266,7 @@ __device__ __forceinline__ void stream_reduce_round(const PipeArgs& a, int4 cT, 
     run = fmaf(val[e], xc[e], run);
     const unsigned rid = rids[e];
     any |= rid;
-    if (!(LB_ABL & 1)) put_y_if<PEERS>(a, yt, rid, i0 - 1, run, rid != 0u && first_rid != 0u);
+    if (!(LB_ABL & 1)) st_cs_if(yt + rid, run, rid != 0u && first_rid != 0u);
     const bool take = rid != 0u && first_rid == 0u;
     first_val = take ? run : first_val;
     first_rid = take ? rid : first_rid;
@@ -1282,7 +1289,7 @@ __device__ __forceinline__ void stream_reduce_round(const PipeArgs& a, int4 cT, 
     const bool lf = (B & ((1u << lane) - 1u)) != 0u;  // a row ended in an earlier lane
     const float carry_in = lane == 0 ? rc : (lf ? lval : rc + lval);
     const int row = i0 - 1 + (int)first_rid;
-    if (!(LB_ABL & 1) || (LB_ABL & 4)) put_y<PEERS>(a, row, carry_in + first_val, row != open_row);
+    if (!(LB_ABL & 1) || (LB_ABL & 4)) put_y<false>(a, row, carry_in + first_val);
   }
   if (any && !(LB_ABL & 4)) tail_clear8(&tail[256 * k + 8 * lane]);
   rc = B ? agg_v : rc + agg_v;
@@ -1297,9 +1304,11 @@ __device__ __forceinline__ void stream_carries_fixup(const PipeArgs& a, int gw, 
     a.carry_row[gw] = i_last;
     a.carry_val[gw] = rc;
   }
-  if (PEERS) __threadfence_system();  // this thread's peer stores are performed before the kernel ends
   __syncthreads();
   if (threadIdx.x == 0) {
+    // the CTA's peer stores (ordered before this thread by the barrier) are performed system-wide
+    // before the kernel ends (fence cumulativity); then the carries are released at GPU scope
+    if (PEERS) __threadfence_system();
     __threadfence();
     const unsigned done = atomicAdd(a.ticket, 1u);
     s_last = done == gridDim.x - 1;
@@ -1369,7 +1378,7 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
     // PEERS: the warp's first row is partial when it started before the warp's first tile (the
     // fix-up completes it and sends it to the peers); every other row this warp writes is final
     const int open_row = PEERS && cT.x < a.rows && cT.y > __ldg(a.off + cT.x) ? cT.x : -1;
-    bool r0e = stream_row_pass<R, K, TailT, PEERS>(a, cT, lane, olo, ohi, tail);
+    bool r0e = stream_row_pass<R, K, TailT>(a, cT, lane, olo, ohi, tail);
     if (t_begin + 1 < t_end) stream_prefetch_offsets<R, K>(a, cT1, lane, olo, ohi);
     __syncwarp();
     // three rounds in flight: reduced (gathered), gathering, loading -- rotated by unrolling the
@@ -1389,14 +1398,16 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_stream_kernel(PipeArgs a) 
         const bool same = k2 < R;
         stream_load(a, same ? cT : cT1, same ? k2 : k2 - R, lane, dl, spol);
       }
-      stream_reduce_round<PEERS>(a, cT, k, lane, r0e, open_row, dc.val, xc, tail, rc);
-      // (e) tile t done: row pass of tile t+1 (offsets prefetched), advance coords
+      stream_reduce_round(a, cT, k, lane, r0e, dc.val, xc, tail, rc);
+      // (e) tile t done: (PEERS) its final rows go to the other ranks, row pass of tile t+1 (offsets
+      // prefetched), advance coords
       if (++k == R) {
         k = 0;
         ++t;
         __syncwarp();
+        if (PEERS) stream_peer_copy(a, cT, open_row, lane);
         if (t < t_end) {
-          r0e = stream_row_pass<R, K, TailT, PEERS>(a, cT1, lane, olo, ohi, tail);
+          r0e = stream_row_pass<R, K, TailT>(a, cT1, lane, olo, ohi, tail);
           if (t + 1 < t_end) stream_prefetch_offsets<R, K>(a, cT2, lane, olo, ohi);
           cT = cT1;
           cT1 = cT2;
