@@ -167,6 +167,41 @@ def time_oracle(sample, seconds: float, min_reps: int = 1):
     return n * reps / dt / 1e9, reps, dt
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_extras(sample, seconds: float) -> dict:
+    """SURVEY 8(d) oracle timing beside the GPU: the single-threaded oracle SpMV and the brute-force
+    (two-pointer walk, O(rows + nnz)) merge-path partitioner on the same sample, each median of up to 5."""
+    import oracle
+    o, c, v, xx, r, n = sample
+
+    def med(fn):
+        ts = []
+        t_end = time.perf_counter() + seconds
+        while len(ts) < 5 and (not ts or time.perf_counter() < t_end):
+            t0 = time.perf_counter()
+            fn()
+            ts.append(time.perf_counter() - t0)
+        return float(np.median(ts)), len(ts)
+
+    t1, n1 = med(lambda: oracle.spmv(o, c, v, xx, threads=False))
+    tp, npart = med(lambda: oracle.partition(o, 1016))
+    return {"cpu_model": cpu_model(), "os_cpu_count": os.cpu_count(),
+            "single_thread": {"value": round(n / t1 / 1e9, 4), "unit": "GNZ/s", "reps": n1,
+                              "timing": "median (oracle.spmv, fp64, 1 thread)"},
+            "partition_bruteforce": {"ms": round(tp * 1e3, 2), "items": int(r + n), "L": 1016, "reps": npart,
+                                     "timing": "median (oracle.partition: two-pointer walk, 1 thread)"}}
+
+
 def run_reference(args, cfg):
     world, rank, local = dist_env()
     if rank != 0:
@@ -315,6 +350,19 @@ def run_single(args, cfg):
                            + ", 256-bit stream loads + gathers, no rows"}
     except Exception as e:  # pragma: no cover
         rec["roofline_gather"] = {"error": str(e)}
+    # the read-only stream rate of this matrix's col_idx + values (no gathers): the in-repo stream
+    # microbenchmark of SURVEY 8(d); the tile kernel's algorithmic GB/s against it
+    try:
+        st_ms = M.probe_stream(reps=20)
+        st_gbs = 8.0 * nnz / (st_ms * 1e-3) / 1e9
+        ach_ph = alg / (float(ph[1]) * 1e-3) / 1e9
+        rec["roofline_stream"] = {
+            "bound": "hbm (read-only stream)", "achieved": round(ach_ph, 1), "peak": round(st_gbs, 1), "unit": "GB/s",
+            "frac": round(ach_ph / st_gbs, 4),
+            "timing": "both right after the timed region: the kernel's phase-call time (algorithmic bytes) vs 20 probe passes",
+            "peak_source": "lb_probe_stream: col_idx + values of this matrix, 256-bit evict-first loads, no gathers"}
+    except Exception as e:  # pragma: no cover
+        rec["roofline_stream"] = {"error": str(e)}
     if plan is not None and no_plan is not None and ms < no_plan["ms_per_step"]:
         plan["break_even_steps"] = int(np.ceil(plan["build_ms"] / (no_plan["ms_per_step"] - ms)))
     if args.no_extras:
@@ -344,6 +392,7 @@ def run_single(args, cfg):
     rec["cpu_baseline"] = {"value": round(gnz, 4), "unit": "GNZ/s", "cores": oracle.num_threads(), "kind": "oracle",
                            "sample": f"leading {sample[4]} rows ({sample[5]} nnz) of {cfg} with full x, {reps} reps "
                                      f"in {dt:.1f} s (oracle.spmv_omp, fp64)"}
+    rec["cpu_baseline"].update(oracle_extras(sample, max(2.0, args.cpu_seconds / 2)))
     print(json.dumps(rec))
 
 
@@ -445,6 +494,15 @@ def run_multi(args, cfg):
     f1.record(stream)
     torch.cuda.synchronize()
     spmv_ms_local = f0.elapsed_time(f1) / args.steps
+    # exchange only (all-gather(v) of y): its time and bus bandwidth per rank
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.barrier()
+    g0.record(stream)
+    for _ in range(args.steps):
+        comm.allgather_rows(b, y)
+    g1.record(stream)
+    torch.cuda.synchronize()
+    ag_ms_local = g0.elapsed_time(g1) / args.steps
     # e2e through the public API: every step copies this rank's shard (CSR arrays) and x from pinned
     # host memory into the handle's borrowed arrays, runs the same multi-GPU step (exchange included)
     # and reads this rank's rows of y back; CUDA events on the stream, max over ranks
@@ -465,12 +523,12 @@ def run_multi(args, cfg):
 
         e2e_step()
         e2e_ms_local = timed(e2e_step, args.e2e_steps)
-    t = torch.tensor([ms_local, spmv_ms_local, e2e_ms_local, float(h2d_local), float(d2h_local)],
+    t = torch.tensor([ms_local, spmv_ms_local, e2e_ms_local, float(h2d_local), float(d2h_local), ag_ms_local],
                      dtype=torch.float64, device=dev)
     tmax = t.clone()
     dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    ms, spmv_ms, e2e_ms = float(tmax[0]), float(tmax[1]), float(tmax[2])
+    ms, spmv_ms, e2e_ms, ag_ms = float(tmax[0]), float(tmax[1]), float(tmax[2]), float(tmax[5])
     h2d_total, d2h_total = int(t[3]), int(t[4])
     if rank == 0:
         rec = {
@@ -486,7 +544,12 @@ def run_multi(args, cfg):
             "plan": plan,
             "no_plan": no_plan,
             "gpu_launches": int(launches),
-            "spmv_only": {"value": round(nnz / (spmv_ms * 1e-3) / 1e9, 3), "unit": "GNZ/s", "ms": round(spmv_ms, 5)},
+            "spmv_only": {"value": round(nnz / (spmv_ms * 1e-3) / 1e9, 3), "unit": "GNZ/s", "ms": round(spmv_ms, 5),
+                          "per_gpu": round(nnz / world / (spmv_ms * 1e-3) / 1e9, 3)},
+            "exchange": {"ms": round(ag_ms, 5), "op": "lb_allgather_rows (NCCL group of ncclBroadcast, root = each rank)",
+                         "bytes_received_per_rank_max": int(4 * (rows - min(int(b[k + 1] - b[k]) for k in range(world)))),
+                         "bus_GB/s": round(4 * (rows - min(int(b[k + 1] - b[k]) for k in range(world))) / (ag_ms * 1e-3) / 1e9, 1)
+                         if ag_ms > 0 else None},
             "e2e": None if args.no_extras else {
                 "value": round(nnz / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GNZ/s", "h2d_bytes_per_step": h2d_total,
                 "d2h_bytes_per_step": d2h_total, "steps": args.e2e_steps,

