@@ -176,9 +176,13 @@ lb_status_t lb_select_schedule(lb_csr_t A, void* stream, lb_schedule_t* out);
  * lb_spmm -- Y = A X for a dense X with n columns (Listing 4: SpMM is SpMV with a loop
  * over the columns of B), on the same merge-path tiles (L = 1016; lb_partition's output at that
  * length is reused).  X: fp32 [cols x n] row-major with leading dimension ldx >= n; Y: fp32
- * [rows x n], leading dimension ldy >= n, overwritten.  Columns are processed in panels of 4 (one
- * 16-byte gather of X[col, c..c+4) per nonzero) when X, Y are 16-byte aligned and ldx, ldy are
- * multiples of 4, otherwise one column at a time.  X and Y must not alias.
+ * [rows x n], leading dimension ldy >= n, overwritten.  Columns are processed in panels: 32 or 16
+ * columns with lanes over columns (lane c of a P-lane group gathers X[col, c]; needs 32-byte
+ * aligned col_idx/values, ldy a multiple of 4 and a 16-byte aligned Y panel), otherwise 8 columns
+ * with one 32-byte gather of X[col, c..c+8) per nonzero (X rows 32-byte aligned), 4 columns with one
+ * 16-byte gather (16-byte aligned, ldx and ldy multiples of 4), or one column at a time.  X and Y must not
+ * alias.  Errors: LB_ERR_INVALID_ARG for a null handle, n < 0, ldx < n, ldy < n, null X / Y with
+ * work to do, or X == Y.
  */
 lb_status_t lb_spmm(lb_csr_t A, int64_t n, const float* d_X, int64_t ldx, float* d_Y, int64_t ldy, void* stream);
 

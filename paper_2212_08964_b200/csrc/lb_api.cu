@@ -52,6 +52,7 @@ constexpr int kNT = 256;
 // nonzero inside the kernels' int32 position arithmetic
 constexpr int64_t kMaxMergeItems = (1ll << 31) - (1ll << 16) - 1;
 constexpr int kMaxCtas = 8192;      // carry slots per handle (>= SMs x resident CTAs)
+constexpr int kCarryVals = 32 * kMaxCtas;  // carry values per handle (SpMM: up to 32 per carry slot)
 constexpr int kMinTile = 504;       // smallest supported L: sizes the partition cache
 
 // Merge-path tile lengths.  The pipelined kernel runs NT threads x E nonzeros per tile, so a
@@ -292,7 +293,7 @@ size_t align256(size_t n) { return (n + 255) & ~size_t(255); }
 
 size_t scratch_bytes(int64_t rows, int64_t nnz) {
   return align256((num_tiles(rows, nnz, kMinTile) + 1) * sizeof(int2)) + align256(kMaxCtas * sizeof(int)) +
-         align256(4 * kMaxCtas * sizeof(float)) + align256(4 * sizeof(int)) + align256(sizeof(unsigned));
+         align256(kCarryVals * sizeof(float)) + align256(4 * sizeof(int)) + align256(sizeof(unsigned));
 }
 
 void carve_scratch(lb_csr_s* A, char* p) {
@@ -301,7 +302,7 @@ void carve_scratch(lb_csr_s* A, char* p) {
   A->carry_row = reinterpret_cast<int*>(p);
   p += align256(kMaxCtas * sizeof(int));
   A->carry_val = reinterpret_cast<float*>(p);
-  p += align256(4 * kMaxCtas * sizeof(float));  // up to 4 values per carry (SpMM panels)
+  p += align256(kCarryVals * sizeof(float));  // up to 32 values per carry (SpMM panels)
   A->flags = reinterpret_cast<int*>(p);
   p += align256(4 * sizeof(int));
   A->ticket = reinterpret_cast<unsigned*>(p);
@@ -1127,8 +1128,8 @@ lb_status_t spmm_panel(lb_csr_s* A, const float* X, int64_t ldx, float* Y, int64
     blocks = std::max(1, blocks);
   }
   const int T = (int)num_tiles(A->rows, A->nnz, kSpmmL);
-  // carry_val holds 4 * kMaxCtas floats: P values per warp
-  const int warps_max = std::min(A->dev->sm_count * blocks * kSpmmW, 4 * kMaxCtas / P);
+  // carry_val holds kCarryVals floats: P values per warp
+  const int warps_max = std::min(A->dev->sm_count * blocks * kSpmmW, std::min(kMaxCtas, kCarryVals / P));
   const int tpw = (T + warps_max - 1) / warps_max;
   const int warps = (T + tpw - 1) / tpw;
   const int grid = (warps + kSpmmW - 1) / kSpmmW;
@@ -1139,6 +1140,45 @@ lb_status_t spmm_panel(lb_csr_s* A, const float* X, int64_t ldx, float* Y, int64
   k<<<grid, kSpmmW * 32, 0, s>>>(a);
   LB_LAUNCHED();
   return LB_OK;
+}
+
+// lanes-over-columns SpMM panel of P = 16/32 columns (merge_spmm_cols_kernel): one CTA of 16 warps per SM
+constexpr int kSpmmColsW = 16;
+template <int P>
+lb_status_t spmm_cols_panel(lb_csr_s* A, const float* X, int64_t ldx, float* Y, int64_t ldy, stream_t s) {
+  auto k = lbk::merge_spmm_cols_kernel<kSpmmColsW, 4, P>;
+  constexpr int dyn = lbk::spmm_cols_dyn_bytes(kSpmmColsW, P);
+  static int blocks_cache[64][3] = {{0}};
+  int& blocks = blocks_cache[A->device][P == 8 ? 0 : P == 16 ? 1 : 2];
+  if (blocks == 0) {
+    cudaFuncAttributes fa;
+    LB_CUDA(cudaFuncGetAttributes(&fa, k));
+    LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+    LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, kSpmmColsW * 32, dyn));
+    const double need = (double)blocks * (fa.sharedSizeBytes + dyn + 1024);
+    int pct = std::min(100, std::max(1, (int)(100.0 * need / (228.0 * 1024.0)) + 1));
+    LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+    LB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, kSpmmColsW * 32, dyn));
+    if (blocks < 1) return fail(LB_ERR_UNSUPPORTED, "SpMM column-panel kernel does not fit");
+  }
+  const int T = (int)num_tiles(A->rows, A->nnz, kSpmmL);
+  const int warps_max = std::min(A->dev->sm_count * blocks * kSpmmColsW, std::min(kMaxCtas, kCarryVals / P));
+  const int tpw = (T + warps_max - 1) / warps_max;
+  const int warps = (T + tpw - 1) / tpw;
+  const int grid = (warps + kSpmmColsW - 1) / kSpmmColsW;
+  lbk::SpmmArgs a;
+  a.off = A->off; a.col = A->col; a.val = A->val; a.X = X; a.Y = Y; a.ldx = ldx; a.ldy = ldy;
+  a.coords = A->coords; a.rows = (int)A->rows; a.nnz = (int)A->nnz; a.num_tiles = T; a.tiles_per_warp = tpw;
+  a.carry_row = A->carry_row; a.carry_val = A->carry_val; a.ticket = A->ticket; a.vec = 1;
+  k<<<grid, kSpmmColsW * 32, dyn, s>>>(a);
+  LB_LAUNCHED();
+  return LB_OK;
+}
+
+// LB_SPMM=lanes (tests and comparison runs only) forces the lanes-over-nonzeros kernel for every panel
+int spmm_mode() {
+  const char* env = getenv("LB_SPMM");
+  return env && strcmp(env, "lanes") == 0 ? 1 : 0;
 }
 
 lb_status_t spmm_impl(lb_csr_s* A, int64_t n, const float* X, int64_t ldx, float* Y, int64_t ldy, stream_t s) {
@@ -1154,7 +1194,22 @@ lb_status_t spmm_impl(lb_csr_s* A, int64_t n, const float* X, int64_t ldx, float
     A->coords_L = kSpmmL;
     A->coords_kind = 0;
   }
+  const int mode = spmm_mode();
+  const bool cols_ok = A->vec32 && ldy % 4 == 0 && mode != 1;
   for (int64_t c0 = 0; c0 < n;) {
+    // lanes over columns: panels of 32 / 16 columns (Y rows 16-byte aligned for the zero-row stores);
+    // measured against the lanes-over-nonzeros kernel (tools/bench_spmm.py,
+    // profiles/r01_spmm_cols_vs_lanes.jsonl): 1.3-1.65x at n = 16 and 1.7-2.1x at n = 32 on C3/C4/C5,
+    // but slower at n = 8 (0.7-0.83x), so 8..15 remaining columns take the 8-column panel below
+    if (cols_ok && n - c0 >= 16 && reinterpret_cast<uintptr_t>(Y + c0) % 16 == 0) {
+      const int64_t left = n - c0;
+      const int P = left >= 32 ? 32 : 16;
+      st = P == 32 ? spmm_cols_panel<32>(A, X + c0, ldx, Y + c0, ldy, s)
+                   : spmm_cols_panel<16>(A, X + c0, ldx, Y + c0, ldy, s);
+      if (st != LB_OK) return st;
+      c0 += P;
+      continue;
+    }
     // 8-column panels gather one 32-byte sector per nonzero (X rows 32-byte aligned)
     const bool oct = n - c0 >= 8 && ldx % 8 == 0 && ldy % 4 == 0 &&
                      reinterpret_cast<uintptr_t>(X + c0) % 32 == 0 && reinterpret_cast<uintptr_t>(Y + c0) % 16 == 0;

@@ -2213,6 +2213,288 @@ __global__ void __launch_bounds__(W * 32, MINB) merge_spmm_kernel(SpmmArgs a) {
   }
 }
 
+// ----------------------------------------------------------------------------- SpMM, lanes over columns
+// Y = A X for a panel of P (8, 16 or 32) columns on the same merge-path tiles (L = 1016): a warp is
+// NG = 32 / P groups of P lanes and lane (g, c) owns column c of the panel.  A round is 32 NG
+// consecutive nonzero positions, 32 per group.  The warp loads the round's col/val coalesced (NG
+// positions per lane, one 16/8/4-byte load each), zeroes the values outside the tile and stages them
+// in a two-slot shared ring; every lane then reads its group's 32 columns / values with broadcast
+// 16-byte shared loads and gathers X[col, c] -- the P lanes of a group read one contiguous 4P-byte
+// segment per nonzero.  Each lane sums its 32 products in one FMA chain, row ends inside the chain are
+// stored directly (P contiguous floats per group), and the open row's partial crosses groups with a
+// log2(NG)-step segmented scan that moves values by P lanes (same column).  Row ends come from the
+// same per-warp marker buffer as SpMV.  Compared with merge_spmm_kernel (lanes over nonzeros, P values
+// per lane), the per-column scans across 32 lanes disappear and a round carries 1024 products.
+template <int P>
+__device__ __forceinline__ void spmm_zero_row(const SpmmArgs& a, int row) {
+  float4* dst = reinterpret_cast<float4*>(a.Y + (int64_t)row * a.ldy);
+#pragma unroll
+  for (int q = 0; q < P / 4; ++q) __stcs(dst + q, make_float4(0.f, 0.f, 0.f, 0.f));
+}
+
+template <int NG>
+struct SpmmColsLoad {  // one lane's share of a round: NG consecutive positions
+  int col[NG];
+  float val[NG];
+};
+
+// dynamic shared memory of merge_spmm_cols_kernel<W, R, P> (the col/val staging ring)
+__host__ __device__ constexpr int spmm_cols_dyn_bytes(int W, int P) { return W * 2 * (32 / P) * 36 * 4 * 2; }
+
+template <int W, int R, int P>
+__global__ void __launch_bounds__(W * 32, 1) merge_spmm_cols_kernel(SpmmArgs a) {
+  static_assert(P == 8 || P == 16 || P == 32, "P");
+  constexpr int NG = 32 / P;              // groups per warp
+  constexpr int EG = 32;                  // positions per group per round
+  constexpr int kCap = 256 * R;           // tile positions (L = kCap - 8)
+  constexpr int RP = EG * NG;             // positions per round
+  constexpr int RT = kCap / RP;           // rounds per tile
+  constexpr int GS = EG + 4;              // padded group stride of the staging ring (words)
+  constexpr int K = 2;
+  __shared__ __align__(16) unsigned short s_tail[W][kCap];
+  __shared__ int s_last;
+  // staging ring in dynamic shared memory: [W][2 slots][NG * GS] columns, then the same for values
+  extern __shared__ __align__(16) int s_dyn[];
+  int (*s_col)[2][NG * GS] = reinterpret_cast<int (*)[2][NG * GS]>(s_dyn);
+  float (*s_val)[2][NG * GS] = reinterpret_cast<float (*)[2][NG * GS]>(s_dyn + W * 2 * NG * GS);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / P, cl = lane % P;
+  const int gw = blockIdx.x * W + warp;
+  const int t_begin = min(a.num_tiles, gw * a.tiles_per_warp);
+  const int t_end = min(a.num_tiles, t_begin + a.tiles_per_warp);
+  const uint64_t spol = policy_evict_first();
+  unsigned short* tail = s_tail[warp];
+  for (int w = lane; w < kCap / 8; w += 32) reinterpret_cast<uint4*>(tail)[w] = make_uint4(0u, 0u, 0u, 0u);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  __syncwarp();
+
+  PipeArgs pa;
+  pa.off = a.off; pa.coords = a.coords; pa.rows = a.rows; pa.nnz = a.nnz;
+  float rc = 0.f;  // partial of the open row, column cl (the same in every group)
+  int i_last = t_begin < t_end ? __ldg(&a.coords[t_end].x) : a.rows;
+  if (t_begin < t_end) {
+    const float* __restrict__ Xc = a.X + cl;
+    const int nsteps = (t_end - t_begin) * RT;
+    int4 cT = tile_coords(pa, t_begin);
+    int4 cT1 = t_begin + 1 < t_end ? tile_coords(pa, t_begin + 1) : cT;
+    int4 cT2 = t_begin + 2 < t_end ? tile_coords(pa, t_begin + 2) : cT1;
+    int olo[K], ohi[K];
+    bool r0e = false;  // (warp-uniform) row i0 of the current tile has no nonzero in it
+    // row pass: marks row ends in tail[], writes the zero rows (rows r > 0 without a nonzero here)
+    auto row_pass = [&](int4 c) -> bool {
+      const int i0 = c.x, nrows = c.z - c.x, jA = c.y & ~7, lo = c.y - jA;
+      bool row0_empty = false;
+      for (int j = 0; 32 * j < nrows; ++j) {
+        const int r = lane + 32 * j;
+        if (r < nrows) {
+          int ob, oe;
+          if (j < K) {
+#pragma unroll
+            for (int q = 0; q < K; ++q)
+              if (q == j) { ob = olo[q]; oe = ohi[q]; }
+          } else {
+            ob = __ldcs(a.off + i0 + r);
+            oe = __ldcs(a.off + i0 + r + 1);
+          }
+          const int e = oe - jA;
+          const int s = r == 0 ? lo : ob - jA;
+          if (e > s) tail[e - 1] = (unsigned short)(r + 1);
+          else if (r > 0) spmm_zero_row<P>(a, i0 + r);
+          else row0_empty = true;
+        }
+      }
+      return __shfl_sync(kFull, (int)row0_empty, 0) != 0;
+    };
+    // this lane's NG positions of round kk of tile c; values outside the tile's nonzero range are 0
+    auto load = [&](int4 c, int kk, SpmmColsLoad<NG>& d) {
+      const int jA = c.y & ~7;
+      const int q0 = RP * kk + NG * lane;  // tile-local position
+      const int g = jA + q0;
+      const int lo = c.y - jA, hi = c.w - jA;
+      if (g + NG <= c.w && g + NG <= a.nnz) {
+        if constexpr (NG == 4) {
+          const int4 ci = ld_cs_v4(a.col + g);
+          const float4 vi = ld_cs_v4(a.val + g);
+          d.col[0] = ci.x; d.col[1] = ci.y; d.col[2] = ci.z; d.col[3] = ci.w;
+          d.val[0] = vi.x; d.val[1] = vi.y; d.val[2] = vi.z; d.val[3] = vi.w;
+        } else if constexpr (NG == 2) {
+          const int2 ci = __ldcs(reinterpret_cast<const int2*>(a.col + g));
+          const float2 vi = __ldcs(reinterpret_cast<const float2*>(a.val + g));
+          d.col[0] = ci.x; d.col[1] = ci.y;
+          d.val[0] = vi.x; d.val[1] = vi.y;
+        } else {
+          d.col[0] = ld_cs(a.col + g);
+          d.val[0] = ld_cs(a.val + g);
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < NG; ++e) {
+          const bool ok = g + e < c.w;
+          d.col[e] = ok ? ld_cs(a.col + g + e) : 0;
+          d.val[e] = ok ? ld_cs(a.val + g + e) : 0.f;
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < NG; ++e)
+        if (q0 + e < lo || q0 + e >= hi) d.val[e] = 0.f;
+    };
+    // stage a loaded round into ring slot sl: position q of the round -> group q / 32, index q % 32
+    auto stage = [&](const SpmmColsLoad<NG>& d, int sl) {
+      const int q = NG * lane, gq = q / EG, eq = q % EG;
+      int* dc = &s_col[warp][sl][gq * GS + eq];
+      float* dv = &s_val[warp][sl][gq * GS + eq];
+      if constexpr (NG == 4) {
+        *reinterpret_cast<int4*>(dc) = make_int4(d.col[0], d.col[1], d.col[2], d.col[3]);
+        *reinterpret_cast<float4*>(dv) = make_float4(d.val[0], d.val[1], d.val[2], d.val[3]);
+      } else if constexpr (NG == 2) {
+        *reinterpret_cast<int2*>(dc) = make_int2(d.col[0], d.col[1]);
+        *reinterpret_cast<float2*>(dv) = make_float2(d.val[0], d.val[1]);
+      } else {
+        *dc = d.col[0];
+        *dv = d.val[0];
+      }
+    };
+    // the group's 32 gathers of the round staged in slot sl
+    auto gather = [&](int sl, float (&xv)[EG]) {
+      const int* sc = &s_col[warp][sl][grp * GS];
+#pragma unroll
+      for (int e = 0; e < EG; e += 4) {
+        const int4 c4 = *reinterpret_cast<const int4*>(sc + e);
+        xv[e] = __ldg(Xc + (int64_t)c4.x * a.ldx);
+        xv[e + 1] = __ldg(Xc + (int64_t)c4.y * a.ldx);
+        xv[e + 2] = __ldg(Xc + (int64_t)c4.z * a.ldx);
+        xv[e + 3] = __ldg(Xc + (int64_t)c4.w * a.ldx);
+      }
+    };
+    auto reduce = [&](int kk, int sl, const float (&xc)[EG]) {
+      const int i0 = cT.x;
+      if (kk == 0 && r0e) {
+        if (grp == 0) a.Y[(int64_t)i0 * a.ldy + cl] = rc;
+        rc = 0.f;
+      }
+      const float* sv = &s_val[warp][sl][grp * GS];
+      const unsigned short* tg = &tail[RP * kk + EG * grp];
+      float* yt = a.Y + (int64_t)(i0 - 1) * a.ldy + cl;  // row r of the tile ends where rid = r + 1
+      unsigned first_rid = 0u;
+      float run = 0.f, first_val = 0.f;
+#pragma unroll
+      for (int e8 = 0; e8 < EG; e8 += 8) {
+        unsigned rids[8];
+        tail_read8(tg + e8, rids);
+        const float4 v0 = *reinterpret_cast<const float4*>(sv + e8);
+        const float4 v1 = *reinterpret_cast<const float4*>(sv + e8 + 4);
+        const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          run = fmaf(vv[e], xc[e8 + e], run);
+          const unsigned rid = rids[e];
+          st_cs_if(yt + (int64_t)rid * a.ldy, run, rid != 0u && first_rid != 0u);
+          const bool take = rid != 0u && first_rid == 0u;
+          first_val = take ? run : first_val;
+          first_rid = take ? rid : first_rid;
+          run = rid != 0u ? 0.f : run;
+        }
+      }
+      // group flags: bit j set when group j has a row end in this round
+      const unsigned B = __ballot_sync(kFull, first_rid != 0u);
+      unsigned GF = 0u;
+#pragma unroll
+      for (int j = 0; j < NG; ++j) GF |= ((B >> (j * P)) & 1u) << j;
+      float v = run;
+#pragma unroll
+      for (int o = 1; o < NG; o <<= 1) {
+        const float vo = __shfl_up_sync(kFull, v, o * P);
+        const bool reset = grp >= o ? ((GF >> (grp - o + 1)) & ((1u << o) - 1u)) != 0u : true;
+        if (!reset) v = vo + v;
+      }
+      const float lval = __shfl_up_sync(kFull, v, P % 32);
+      const float agg_v = __shfl_sync(kFull, v, (NG - 1) * P + cl);
+      if (first_rid != 0u) {
+        const bool lf = (GF & ((1u << grp) - 1u)) != 0u;  // a row ended in an earlier group
+        const float carry_in = grp == 0 ? rc : (lf ? lval : rc + lval);
+        a.Y[(int64_t)(i0 - 1 + (int)first_rid) * a.ldy + cl] = carry_in + first_val;
+      }
+      rc = GF ? agg_v : rc + agg_v;
+    };
+    stream_prefetch_offsets<R, K>(pa, cT, lane, olo, ohi);
+    r0e = row_pass(cT);
+    if (t_begin + 1 < t_end) stream_prefetch_offsets<R, K>(pa, cT1, lane, olo, ohi);
+    // pipeline: step st stages round st+1 (loaded during step st-1) and issues its gathers, loads
+    // round st+2 into registers, and reduces round st (staged and gathered during step st-1)
+    SpmmColsLoad<NG> ld;
+    float X0[EG], X1[EG];
+    load(cT, 0, ld);
+    stage(ld, 0);
+    if (1 < nsteps) load(RT > 1 ? cT : cT1, RT > 1 ? 1 : 0, ld);
+    __syncwarp();
+    gather(0, X0);
+    int t = t_begin, k = 0, st = 0;
+    auto step = [&](float (&xc)[EG], float (&xn)[EG]) {
+      const int sl = st & 1;
+      if (st + 1 < nsteps) {
+        stage(ld, sl ^ 1);
+        __syncwarp();
+        gather(sl ^ 1, xn);
+      }
+      if (st + 2 < nsteps) {
+        const int k2 = k + 2;
+        const int4 c2 = k2 < RT ? cT : (k2 < 2 * RT ? cT1 : cT2);
+        load(c2, k2 < RT ? k2 : (k2 < 2 * RT ? k2 - RT : k2 - 2 * RT), ld);
+      }
+      reduce(k, sl, xc);
+      if (++k == RT) {
+        k = 0;
+        ++t;
+        __syncwarp();
+        for (int w = lane; w < kCap / 8; w += 32) reinterpret_cast<uint4*>(tail)[w] = make_uint4(0u, 0u, 0u, 0u);
+        __syncwarp();
+        if (t < t_end) {
+          r0e = row_pass(cT1);
+          if (t + 1 < t_end) stream_prefetch_offsets<R, K>(pa, cT2, lane, olo, ohi);
+          cT = cT1;
+          cT1 = cT2;
+          if (t + 2 < t_end) cT2 = tile_coords(pa, t + 2);
+        }
+      }
+      __syncwarp();
+    };
+    while (true) {
+      step(X0, X1);
+      if (++st == nsteps) break;
+      step(X1, X0);
+      if (++st == nsteps) break;
+    }
+  }
+
+  if (grp == 0) {
+    if (cl == 0) a.carry_row[gw] = i_last;
+    a.carry_val[(int64_t)gw * P + cl] = rc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned done = atomicAdd(a.ticket, 1u);
+    s_last = done == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    const int nc = (int)gridDim.x * W;
+    // one (carry, column) pair per thread: carries of equal rows are summed in warp order
+    for (int u = threadIdx.x; u < nc * P; u += W * 32) {
+      const int c = u / P, j = u % P;
+      const int r = __ldcg(a.carry_row + c);
+      if (r >= a.rows) continue;
+      if (c > 0 && __ldcg(a.carry_row + c - 1) == r) continue;
+      float sum = 0.f;
+      for (int kk = c; kk < nc && __ldcg(a.carry_row + kk) == r; ++kk) sum += __ldcg(a.carry_val + (int64_t)kk * P + j);
+      float* dst = a.Y + (int64_t)r * a.ldy + j;
+      *dst = __ldcg(dst) + sum;
+    }
+    if (threadIdx.x == 0) *a.ticket = 0u;
+  }
+}
+
 // ----------------------------------------------------------------------------- thread-mapped
 // Listing 3: for row in tiles() (grid-stride, Listing 2), for nz in
 // atoms(row): sum += values[nz] * x[indices[nz]]; y[row] = sum.  Four independent partial

@@ -12,6 +12,8 @@ sampled rows for C5).
 """
 import ctypes
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -464,9 +466,14 @@ def check_Y(Y_gpu, Y_ref, S_ref, exact, what=""):
         assert np.all(err <= TOL * S_ref + 1e-30), f"{what}: worst rel {np.max(err / (S_ref + 1e-30)):.3e}"
 
 
-@pytest.mark.parametrize("n", [1, 3, 4, 5, 8, 16])
+@pytest.mark.parametrize("kernel", ["default", "lanes"])
+@pytest.mark.parametrize("n", [1, 3, 4, 5, 8, 16, 24, 32, 45])
 @pytest.mark.parametrize("name", ["rmat12", "stencil100", "skewed", "c1"])
-def test_spmm_parity(name, n):
+def test_spmm_parity(name, n, kernel, monkeypatch):
+    """Both SpMM tile processors: lanes over columns (merge_spmm_cols_kernel, panels of 32/16) and
+    lanes over nonzeros (merge_spmm_kernel: panels of 8/4/1; every panel with LB_SPMM=lanes)."""
+    if kernel != "default":
+        monkeypatch.setenv("LB_SPMM", kernel)
     for vm in ("int", "float"):
         A = SMALL[name](vm)
         X = lbgen.make_x(A.cols * n, vm, 21).reshape(A.cols, n)
@@ -492,10 +499,28 @@ def test_spmm_strided_and_edge_cases():
         Y_ref, S_ref = oracle.spmm(A.row_offsets, A.col_idx, A.values, Xv.cpu().contiguous())
         check_Y(M.spmm(Xv), Y_ref, S_ref, True, f"ldx16[{lo}:{hi}]")
     for nm, B in {"giant": _csr([0, 50_001], 1), "no_nnz": _csr([0] * 2001, 3),
-                  "golden": _csr([0, 1, 3, 3, 6], 1)}.items():
-        X = torch.ones(B.cols, 4)
-        Y_ref, S_ref = oracle.spmm(B.row_offsets, B.col_idx, B.values, X)
-        check_Y(lb.CsrMatrix.from_csr(B).spmm(X.cuda()), Y_ref, S_ref, True, nm)
+                  "golden": _csr([0, 1, 3, 3, 6], 1),
+                  "giant_mid": _csr([0, 0, 3, 40_003, 40_003, 40_010] + [40_010] * 700, 5),
+                  "empty_runs": _csr([0] + [0] * 3000 + [2] + [2] * 5000 + [9], 7)}.items():
+        for n in (4, 8, 16, 32):
+            X = lbgen.make_x(B.cols * n, "int", 9).reshape(B.cols, n)
+            Y_ref, S_ref = oracle.spmm(B.row_offsets, B.col_idx, B.values, X)
+            for mode in ("default", "lanes"):
+                if mode == "lanes":
+                    os.environ["LB_SPMM"] = "lanes"
+                try:
+                    check_Y(lb.CsrMatrix.from_csr(B).spmm(X.cuda()), Y_ref, S_ref, True, f"{nm}/n={n}/{mode}")
+                finally:
+                    os.environ.pop("LB_SPMM", None)
+    # Y with a leading dimension (ldy = 40) and a misaligned Y view (Y + 1: scalar fallback panels)
+    X = lbgen.make_x(A.cols * 32, "int", 10).reshape(A.cols, 32).cuda()
+    Y_ref, S_ref = oracle.spmm(A.row_offsets, A.col_idx, A.values, X.cpu())
+    for off in (0, 1, 4):
+        Ybig = torch.full((A.rows, 40), 7.0, device="cuda")
+        Yv = Ybig[:, off:off + 32]
+        M.spmm(X, Yv)
+        check_Y(Yv, Y_ref, S_ref, True, f"ldy40+{off}")
+        assert torch.all(Ybig[:, :off] == 7.0) and torch.all(Ybig[:, off + 32:] == 7.0), "wrote outside the view"
     # SpMM column j equals SpMV with x = X[:, j] (same tiles, same arithmetic per column)
     A = lbgen.rmat(12, 16, 8, "float")
     X = lbgen.make_x(A.cols * 4, "float", 5).reshape(A.cols, 4).cuda()
@@ -505,7 +530,7 @@ def test_spmm_strided_and_edge_cases():
     check_Y(Y, Y_ref, S_ref, False, "float n=4")
 
 
-@pytest.mark.parametrize("cfg,n", [("c3", 4), ("c4", 4), ("c3", 8)])
+@pytest.mark.parametrize("cfg,n", [("c3", 4), ("c4", 4), ("c3", 8), ("c3", 16), ("c4", 32)])
 def test_spmm_full_size(cfg, n):
     """Full-size SpMM: 4-column panels, and an 8-column panel (one 256-bit gather per nonzero)."""
     torch.cuda.empty_cache()
