@@ -1195,7 +1195,7 @@ lb_status_t spmm_impl(lb_csr_s* A, int64_t n, const float* X, int64_t ldx, float
     A->coords_kind = 0;
   }
   const int mode = spmm_mode();
-  const bool cols_ok = A->vec32 && ldy % 4 == 0 && mode != 1;
+  const bool cols_ok = A->vec32 && ldy % 4 == 0 && ldx <= INT32_MAX && ldy <= INT32_MAX && mode != 1;
   for (int64_t c0 = 0; c0 < n;) {
     // lanes over columns: panels of 32 / 16 columns (Y rows 16-byte aligned for the zero-row stores);
     // measured against the lanes-over-nonzeros kernel (tools/bench_spmm.py,

@@ -2355,15 +2355,16 @@ __global__ void __launch_bounds__(W * 32, 1) merge_spmm_cols_kernel(SpmmArgs a) 
       }
     };
     // the group's 32 gathers of the round staged in slot sl
+    const int ldx = (int)a.ldx, ldy = (int)a.ldy;  // < 2^31 (checked by the launcher): one IMAD.WIDE per address
     auto gather = [&](int sl, float (&xv)[EG]) {
       const int* sc = &s_col[warp][sl][grp * GS];
 #pragma unroll
       for (int e = 0; e < EG; e += 4) {
         const int4 c4 = *reinterpret_cast<const int4*>(sc + e);
-        xv[e] = __ldg(Xc + (int64_t)c4.x * a.ldx);
-        xv[e + 1] = __ldg(Xc + (int64_t)c4.y * a.ldx);
-        xv[e + 2] = __ldg(Xc + (int64_t)c4.z * a.ldx);
-        xv[e + 3] = __ldg(Xc + (int64_t)c4.w * a.ldx);
+        xv[e] = __ldg(Xc + (int64_t)c4.x * ldx);
+        xv[e + 1] = __ldg(Xc + (int64_t)c4.y * ldx);
+        xv[e + 2] = __ldg(Xc + (int64_t)c4.z * ldx);
+        xv[e + 3] = __ldg(Xc + (int64_t)c4.w * ldx);
       }
     };
     auto reduce = [&](int kk, int sl, const float (&xc)[EG]) {
@@ -2374,25 +2375,30 @@ __global__ void __launch_bounds__(W * 32, 1) merge_spmm_cols_kernel(SpmmArgs a) 
       }
       const float* sv = &s_val[warp][sl][grp * GS];
       const unsigned short* tg = &tail[RP * kk + EG * grp];
-      float* yt = a.Y + (int64_t)(i0 - 1) * a.ldy + cl;  // row r of the tile ends where rid = r + 1
+      float* yt = a.Y + (int64_t)(i0 - 1) * ldy + cl;  // row r of the tile ends where rid = r + 1
       unsigned first_rid = 0u;
       float run = 0.f, first_val = 0.f;
 #pragma unroll
       for (int e8 = 0; e8 < EG; e8 += 8) {
-        unsigned rids[8];
-        tail_read8(tg + e8, rids);
+        const uint4 tq = *reinterpret_cast<const uint4*>(tg + e8);
         const float4 v0 = *reinterpret_cast<const float4*>(sv + e8);
         const float4 v1 = *reinterpret_cast<const float4*>(sv + e8 + 4);
         const float vv[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        if ((tq.x | tq.y | tq.z | tq.w) == 0u) {  // no row ends in these 8 (group-uniform): FMAs only
+#pragma unroll
+          for (int e = 0; e < 8; ++e) run = fmaf(vv[e], xc[e8 + e], run);
+          continue;
+        }
+        const unsigned w4[4] = {tq.x, tq.y, tq.z, tq.w};
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           run = fmaf(vv[e], xc[e8 + e], run);
-          const unsigned rid = rids[e];
-          st_cs_if(yt + (int64_t)rid * a.ldy, run, rid != 0u && first_rid != 0u);
-          const bool take = rid != 0u && first_rid == 0u;
-          first_val = take ? run : first_val;
-          first_rid = take ? rid : first_rid;
-          run = rid != 0u ? 0.f : run;
+          const unsigned rid = (e & 1) ? (w4[e >> 1] >> 16) : (w4[e >> 1] & 0xFFFFu);
+          if (rid != 0u) {  // group-uniform
+            if (first_rid != 0u) __stcs(yt + (int64_t)(int)rid * ldy, run);
+            else { first_val = run; first_rid = rid; }
+            run = 0.f;
+          }
         }
       }
       // group flags: bit j set when group j has a row end in this round
