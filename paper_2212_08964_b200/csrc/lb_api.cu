@@ -278,6 +278,7 @@ struct lb_csr_s {
   int* fo = nullptr;           // [rows + 1] frontier degree prefix (merge-path)
   int* bsum = nullptr;         // [rows / kScanChunk + 2] scan block sums
   int* counts = nullptr;       // [4] frontier size, next size, negative-weight flag
+  int* tc = nullptr;           // [(rows + nnz) / kSsspTile + 2] tile boundaries of a merge-path round
   // BINNING workspace (allocated on first use): [CTA | warp | thread] bin row ids, per-block counts
   void* bin_mem = nullptr;
   int* bin_ids = nullptr;      // [rows]
@@ -1047,8 +1048,9 @@ lb_status_t sssp_impl(lb_csr_s* A, int64_t source, lb_schedule_t sched, float* d
   const int n = (int)A->rows;
   const int nb_max = n / lbk::kScanChunk + 2;
   if (!A->sssp_mem) {
+    const size_t ntc = (size_t)((n + A->nnz) / lbk::kSsspTile + 2);  // tile boundaries of the largest round
     const size_t bytes = 3 * align256((size_t)n * 4) + align256(((size_t)n + 1) * 4) + align256((size_t)nb_max * 4 + 4) +
-                         align256(16);
+                         align256(16) + align256(ntc * 4);
     void* p = nullptr;
     if (cudaMalloc(&p, bytes) != cudaSuccess) { cudaGetLastError(); return fail(LB_ERR_OOM, "SSSP workspace"); }
     char* q = static_cast<char*>(p);
@@ -1058,7 +1060,8 @@ lb_status_t sssp_impl(lb_csr_s* A, int64_t source, lb_schedule_t sched, float* d
     A->stamp = reinterpret_cast<int*>(q); q += align256((size_t)n * 4);
     A->fo = reinterpret_cast<int*>(q); q += align256(((size_t)n + 1) * 4);
     A->bsum = reinterpret_cast<int*>(q); q += align256((size_t)nb_max * 4 + 4);
-    A->counts = reinterpret_cast<int*>(q);
+    A->counts = reinterpret_cast<int*>(q); q += align256(16);
+    A->tc = reinterpret_cast<int*>(q);
   }
   const int sms = A->dev->sm_count;
   lbk::sssp_init_kernel<<<sms * 8, kNT, 0, s>>>(n, (int)source, dist, A->stamp, A->q_a, A->counts);
@@ -1094,10 +1097,15 @@ lb_status_t sssp_impl(lb_csr_s* A, int64_t source, lb_schedule_t sched, float* d
       LB_LAUNCHED();
       lbk::frontier_deg_scan_kernel<<<nb, 256, 0, s>>>(F, qi, A->off, A->bsum, nb, A->fo);
       LB_LAUNCHED();
-      constexpr int kIpt = 16;  // merge items per thread
-      const int grid = sms * 8;
+      // the round's CTA tiles: boundaries in parallel (host-side tile count from F + E_f is not known
+      // without a sync, so the boundary kernel covers the largest possible count and each tile kernel
+      // CTA stops at F + E_f)
+      const int T = (int)((F + A->nnz + lbk::kSsspTile - 1) / lbk::kSsspTile);
+      lbk::sssp_tile_coords_kernel<<<(T + 1 + 255) / 256, 256, 0, s>>>(F, A->fo, T, A->tc);
+      LB_LAUNCHED();
+      const int grid = sms * 8;  // persistent over the round's CTA tiles
       lbk::sssp_merge_kernel<<<grid, kNT, 0, s>>>(F, qi, A->fo, A->off, A->col, A->val, dist, A->stamp, round, qo,
-                                                  A->counts + 1, kIpt);
+                                                  A->counts + 1, A->tc);
       LB_LAUNCHED();
     }
     LB_CUDA(cudaMemcpyAsync(&F, A->counts + 1, sizeof(int), cudaMemcpyDeviceToHost, s));

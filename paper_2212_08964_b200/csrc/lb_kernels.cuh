@@ -1801,45 +1801,98 @@ __global__ void sssp_warp_kernel(int F, const int* __restrict__ q_in, const int*
   }
 }
 
-// merge-path over the frontier: items = F frontier "row ends" + E_f edges, fo = exclusive degree
-// prefix of the frontier (fo[F] = E_f); each thread takes `ipt` consecutive merge items found by the
-// 2-D search (Alg.3) and walks them, relaxing the edges it meets (no reduction, no fix-up).
-__global__ void sssp_merge_kernel(int F, const int* __restrict__ q_in, const int* __restrict__ fo,
-                                  const int* __restrict__ off, const int* __restrict__ col,
-                                  const float* __restrict__ w, float* __restrict__ dist, int* __restrict__ stamp,
-                                  int round, int* __restrict__ q_out, int* __restrict__ n_out, int ipt) {
+// Merge-path relaxation over CTA tiles (Listing 5 P:1076-1107 with Alg.3's split): the merge items of a
+// round are the frontier vertices' ends and their out-edges (edge k of the round belongs to frontier
+// vertex i with fo[i] <= k < fo[i+1]); CTA tile t takes items [t*kSsspTile, (t+1)*kSsspTile).  Thread
+// 0 finds the tile's (vertex, edge) start and end by the 2-D search; the tile's frontier vertices are
+// staged in shared memory (fo[i], off[u] - fo[i], dist[u]); each thread then takes 8 consecutive edges
+// of the tile -- one shared-memory binary search for its first edge's vertex, then a forward walk --
+// so a warp reads 256 consecutive edges' col/w (coalesced within each adjacency list) and issues the
+// 8 edges' loads before relaxing them.  A stale (larger) dist[u] snapshot is harmless: a vertex whose
+// distance drops during the round is pushed and re-relaxes its edges next round.
+constexpr int kSsspTile = 2048;  // merge items per CTA tile (256 threads x 8)
+
+__device__ __forceinline__ int sssp_diag(int F, int Ef, const int* __restrict__ fo, int64_t d) {
+  // i = #{k < F : k + fo[k+1] < d}
+  int lo = (int)(d - Ef > 0 ? d - Ef : 0), hi = (int)(d < F ? d : F);
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((int64_t)mid + __ldcg(fo + mid + 1) < d) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// tile boundaries of a round: tc[t] = frontier index of diagonal min(t kSsspTile, F + E_f), t = 0..T
+// (one thread per boundary, all searches in parallel)
+__global__ void __launch_bounds__(256) sssp_tile_coords_kernel(int F, const int* __restrict__ fo, int T,
+                                                               int* __restrict__ tc) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t > T) return;
   const int Ef = __ldcg(fo + F);
   const int64_t total = (int64_t)F + Ef;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x * ipt;
-  for (int64_t d0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * ipt; d0 < total; d0 += stride) {
-    const int64_t d1 = d0 + ipt < total ? d0 + ipt : total;
-    // 2-D search on diagonal d0: i = #{k < F : k + fo[k+1] < d0}
-    int lo = (int)(d0 - Ef > 0 ? d0 - Ef : 0), hi = (int)(d0 < F ? d0 : F);
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if ((int64_t)mid + __ldcg(fo + mid + 1) < d0) lo = mid + 1; else hi = mid;
+  const int64_t d = (int64_t)t * kSsspTile < total ? (int64_t)t * kSsspTile : total;
+  tc[t] = sssp_diag(F, Ef, fo, d);
+}
+
+__global__ void __launch_bounds__(256) sssp_merge_kernel(int F, const int* __restrict__ q_in,
+                                                         const int* __restrict__ fo, const int* __restrict__ off,
+                                                         const int* __restrict__ col, const float* __restrict__ w,
+                                                         float* __restrict__ dist, int* __restrict__ stamp, int round,
+                                                         int* __restrict__ q_out, int* __restrict__ n_out,
+                                                         const int* __restrict__ tc) {
+  __shared__ int s_fo[kSsspTile + 2];
+  __shared__ int s_base[kSsspTile + 1];
+  __shared__ float s_du[kSsspTile + 1];
+  const int tid = threadIdx.x;
+  const int Ef = __ldcg(fo + F);
+  const int64_t total = (int64_t)F + Ef;
+  for (int64_t t = blockIdx.x; t * kSsspTile < total; t += gridDim.x) {
+    const int64_t d0 = t * kSsspTile, d1 = d0 + kSsspTile < total ? d0 + kSsspTile : total;
+    const int i0 = __ldcg(tc + t), i1 = __ldcg(tc + t + 1);
+    const int j0 = (int)(d0 - i0), j1 = (int)(d1 - i1);
+    const int nv = (i1 < F ? i1 : F - 1) - i0 + 1;  // frontier vertices touched: i0 .. min(i1, F-1)
+    for (int q = tid; q < nv; q += 256) {
+      const int i = i0 + q, u = q_in[i], f = __ldcg(fo + i);
+      s_fo[q] = f;
+      s_base[q] = __ldg(off + u) - f;
+      s_du[q] = __ldcg(dist + u);
     }
-    int i = lo;
-    int j = (int)(d0 - lo);
-    int u = i < F ? q_in[i] : 0;
-    int base = i < F ? __ldg(off + u) - __ldcg(fo + i) : 0;
-    int iend = i < F ? __ldcg(fo + i + 1) : Ef;
-    float du = i < F ? __ldcg(dist + u) : 0.f;
-    for (int64_t d = d0; d < d1; ++d) {
-      if (i < F && j < iend) {  // an edge of frontier vertex i
-        const int e = base + j;
-        sssp_relax(__ldg(col + e), du + __ldg(w + e), dist, stamp, round, q_out, n_out);
-        ++j;
-      } else {  // the end of frontier vertex i
-        ++i;
-        if (i < F) {
-          u = q_in[i];
-          base = __ldg(off + u) - __ldcg(fo + i);
-          iend = __ldcg(fo + i + 1);
-          du = __ldcg(dist + u);
+    if (tid == 0) s_fo[nv > 0 ? nv : 0] = i0 + nv <= F - 1 ? __ldcg(fo + i0 + nv) : Ef;
+    __syncthreads();
+    const int k0 = j0 + 8 * tid;
+    if (nv > 0 && k0 < j1) {
+      // vertex of edge k0: the last q with s_fo[q] <= k0
+      int lo = 0, hi = nv;  // answer in [0, nv)
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (s_fo[mid] <= k0) lo = mid; else hi = mid;
+      }
+      int q = lo;
+      int ev[8];
+      float dv[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int k = k0 + e;
+        if (k < j1) {
+          while (s_fo[q + 1] <= k) ++q;
+          ev[e] = s_base[q] + k;
+          dv[e] = s_du[q];
+        } else {
+          ev[e] = -1;
         }
       }
+      int cv[8];
+      float wv[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        cv[e] = ev[e] >= 0 ? __ldg(col + ev[e]) : 0;
+        wv[e] = ev[e] >= 0 ? __ldg(w + ev[e]) : 0.f;
+      }
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (ev[e] >= 0) sssp_relax(cv[e], dv[e] + wv[e], dist, stamp, round, q_out, n_out);
     }
+    __syncthreads();
   }
 }
 
