@@ -14,8 +14,8 @@
  *    calls are in flight.  A handle owns only its scratch (partition cache, carries), which is
  *    allocated at create time so that lb_spmv can be captured in a CUDA graph.
  *  - Asynchrony: every call is stream-ordered and does not synchronise the host, except
- *    lb_csr_create(validate=1) (one sync to read the validation flag), lb_spmv_host (returns
- *    with y on the host) and the lb_comm_* setup calls.
+ *    lb_csr_create(validate=1) (one sync to read the validation flag), lb_spmv_host and
+ *    lb_spmv_host_x (return with y on the host) and the lb_comm_* setup calls.
  *  - Errors: a status code is returned; no exception crosses the ABI.  lb_last_error()
  *    returns a thread-local message for the last failing call on this thread.
  *  - Index widths: int32 row offsets and column indices, fp32 values, x and y (P:963-969,
@@ -280,6 +280,18 @@ size_t lb_spmv_host_workspace_size(int64_t rows, int64_t cols, int64_t nnz);
 lb_status_t lb_spmv_host(int64_t rows, int64_t cols, int64_t nnz, const int32_t* h_row_offsets,
                          const int32_t* h_col_idx, const float* h_values, const float* h_x, float* h_y,
                          lb_schedule_t sched, void* d_workspace, size_t workspace_bytes, void* stream);
+
+/*
+ * lb_spmv_host_x -- end-to-end y = A x for a device-resident matrix with HOST x and y (the
+ * iterative-solver call: A is uploaded once, every call moves only x in and y out): copies h_x
+ * [cols] host->device into a staging buffer the handle owns (allocated on the first call, freed
+ * by lb_csr_destroy), runs `sched` with `flags` (as lb_spmv_ex), copies y [rows] device->host
+ * into h_y and synchronises `stream` before returning.  Pinned host buffers give full PCIe
+ * bandwidth.  Errors: LB_ERR_INVALID_ARG (null handle, null h_x / h_y with work to do),
+ * LB_ERR_OOM (staging allocation), LB_ERR_CUDA; the schedule's own errors as lb_spmv.
+ */
+lb_status_t lb_spmv_host_x(lb_csr_t A, lb_schedule_t sched, const float* h_x, float* h_y, uint32_t flags,
+                           void* stream);
 
 /*
  * lb_spmv_phase_times -- diagnostics: run `sched` once with CUDA events between its kernels on

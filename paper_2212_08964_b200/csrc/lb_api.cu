@@ -272,6 +272,7 @@ struct lb_csr_s {
   int64_t warm_nnz = 0;
   // SSSP workspace (lb_sssp; allocated on first use)
   void* sssp_mem = nullptr;
+  float* hx_stage = nullptr;   // [cols + rows] device staging of lb_spmv_host_x (x, then y)
   int* q_a = nullptr;          // [rows] frontier lists (ping-pong)
   int* q_b = nullptr;
   int* stamp = nullptr;        // [rows] round of the last push
@@ -1333,6 +1334,7 @@ lb_status_t lb_csr_destroy(lb_csr_t A) {
   if (A->plan_mem) cudaFree(A->plan_mem);
   if (A->sssp_mem) cudaFree(A->sssp_mem);
   if (A->bin_mem) cudaFree(A->bin_mem);
+  if (A->hx_stage) cudaFree(A->hx_stage);
   delete A;
   return LB_OK;
 }
@@ -1529,6 +1531,32 @@ lb_status_t lb_spmv_phase_times(lb_csr_t A, lb_schedule_t sched, const float* d_
   }
   for (auto& e : pe.ev) cudaEventDestroy(e);
   return st;
+}
+
+lb_status_t lb_spmv_host_x(lb_csr_t A, lb_schedule_t sched, const float* h_x, float* h_y, uint32_t flags,
+                           void* stream) {
+  g_err.clear();
+  if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
+  if (A->rows == 0) return LB_OK;
+  if (!h_y || (!h_x && A->cols > 0)) return fail(LB_ERR_INVALID_ARG, "null host x or y");
+  if (!A->hx_stage) {
+    void* p = nullptr;
+    // x and y separately aligned (256 B) inside one allocation
+    if (cudaMalloc(&p, align256((size_t)A->cols * 4) + (size_t)A->rows * 4) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(LB_ERR_OOM, "lb_spmv_host_x staging");
+    }
+    A->hx_stage = static_cast<float*>(p);
+  }
+  stream_t s = S(stream);
+  float* d_x = A->hx_stage;
+  float* d_y = reinterpret_cast<float*>(reinterpret_cast<char*>(A->hx_stage) + align256((size_t)A->cols * 4));
+  if (A->cols > 0) LB_CUDA(cudaMemcpyAsync(d_x, h_x, (size_t)A->cols * 4, cudaMemcpyHostToDevice, s));
+  lb_status_t st = spmv_impl(A, sched, d_x, d_y, flags, s, nullptr);
+  if (st != LB_OK) return st;
+  LB_CUDA(cudaMemcpyAsync(h_y, d_y, (size_t)A->rows * 4, cudaMemcpyDeviceToHost, s));
+  LB_CUDA(cudaStreamSynchronize(s));
+  return LB_OK;
 }
 
 size_t lb_spmv_host_workspace_size(int64_t rows, int64_t cols, int64_t nnz) {

@@ -288,6 +288,31 @@ def test_spmv_host_end_to_end(sched):
     check_y(y, y_ref, s_ref, True, "host")
 
 
+@pytest.mark.parametrize("sched", SCHEDS)
+def test_spmv_host_x_resident_matrix(sched):
+    """lb_spmv_host_x: device-resident A, host x / y (pinned and pageable), repeated calls with new x,
+    with and without the x-reuse plan; bit-exact in integer mode."""
+    A = lbgen.rmat(13, 16, 6, "int")
+    M = lb.CsrMatrix.from_csr(A)
+    for it, pinned in enumerate((True, False, True)):
+        x = lbgen.make_x(A.cols, "int", 20 + it)
+        y_ref, s_ref = ref(A, x)
+        hx = x.pin_memory() if pinned else x.clone()
+        hy = torch.full((A.rows,), float("nan"))
+        hy = hy.pin_memory() if pinned else hy
+        M.spmv_host(hx, hy, sched, repartition=it == 0)
+        check_y(hy, y_ref, s_ref, True, f"host_x/{sched}/{it}")
+    if sched == "merge_path":
+        M.plan_hot_x(256, 1000)
+        x = lbgen.make_x(A.cols, "int", 40)
+        y_ref, s_ref = ref(A, x)
+        hy = torch.empty(A.rows)
+        M.spmv_host(x, hy, sched, repartition=True)
+        check_y(hy, y_ref, s_ref, True, "host_x/plan")
+    with pytest.raises(ValueError):
+        M.spmv_host(torch.zeros(A.cols + 1), torch.zeros(A.rows), sched)
+
+
 @pytest.mark.parametrize("G", [2, 3, 8])
 def test_row_shards_concatenate_bit_identical(G):
     """G equal-nnz shards run one after another on one GPU, concatenated,
