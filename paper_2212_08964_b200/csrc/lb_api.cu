@@ -1185,6 +1185,10 @@ lb_status_t spmm_cols_panel(lb_csr_s* A, const float* X, int64_t ldx, float* Y, 
 }
 
 // LB_SPMM=lanes (tests and comparison runs only) forces the lanes-over-nonzeros kernel for every panel
+#ifndef LB_SPMM_COLS_MIN
+#define LB_SPMM_COLS_MIN 16  // narrowest panel the lanes-over-columns kernel takes (8 or 16)
+#endif
+
 int spmm_mode() {
   const char* env = getenv("LB_SPMM");
   return env && strcmp(env, "lanes") == 0 ? 1 : 0;
@@ -1210,11 +1214,12 @@ lb_status_t spmm_impl(lb_csr_s* A, int64_t n, const float* X, int64_t ldx, float
     // measured against the lanes-over-nonzeros kernel (tools/bench_spmm.py,
     // profiles/r01_spmm_cols_vs_lanes.jsonl): 1.3-1.65x at n = 16 and 1.7-2.1x at n = 32 on C3/C4/C5,
     // but slower at n = 8 (0.7-0.83x), so 8..15 remaining columns take the 8-column panel below
-    if (cols_ok && n - c0 >= 16 && reinterpret_cast<uintptr_t>(Y + c0) % 16 == 0) {
+    if (cols_ok && n - c0 >= LB_SPMM_COLS_MIN && reinterpret_cast<uintptr_t>(Y + c0) % 16 == 0) {
       const int64_t left = n - c0;
-      const int P = left >= 32 ? 32 : 16;
+      const int P = left >= 32 ? 32 : left >= 16 ? 16 : 8;
       st = P == 32 ? spmm_cols_panel<32>(A, X + c0, ldx, Y + c0, ldy, s)
-                   : spmm_cols_panel<16>(A, X + c0, ldx, Y + c0, ldy, s);
+         : P == 16 ? spmm_cols_panel<16>(A, X + c0, ldx, Y + c0, ldy, s)
+                   : spmm_cols_panel<8>(A, X + c0, ldx, Y + c0, ldy, s);
       if (st != LB_OK) return st;
       c0 += P;
       continue;

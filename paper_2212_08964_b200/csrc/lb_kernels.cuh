@@ -2291,6 +2291,9 @@ struct SpmmColsLoad {  // one lane's share of a round: NG consecutive positions
   float val[NG];
 };
 
+#ifndef LB_SPMM_ROTATE
+#define LB_SPMM_ROTATE 0  // merge_spmm_cols_kernel: 1 = two rotated copies of the step (no register copies)
+#endif
 // dynamic shared memory of merge_spmm_cols_kernel<W, R, P> (the col/val staging ring)
 __host__ __device__ constexpr int spmm_cols_dyn_bytes(int W, int P) { return W * 2 * (32 / P) * 36 * 4 * 2; }
 
@@ -2517,12 +2520,22 @@ __global__ void __launch_bounds__(W * 32, 1) merge_spmm_cols_kernel(SpmmArgs a) 
       }
       __syncwarp();
     };
+#if LB_SPMM_ROTATE
     while (true) {
       step(X0, X1);
       if (++st == nsteps) break;
       step(X1, X0);
       if (++st == nsteps) break;
     }
+#else
+    // one copy of the step (the code of a round is large: two rotated copies thrash the instruction
+    // cache), the gathered round moved into place with register copies
+    for (; st < nsteps; ++st) {
+      step(X0, X1);
+#pragma unroll
+      for (int e = 0; e < EG; ++e) X0[e] = X1[e];
+    }
+#endif
   }
 
   if (grp == 0) {
