@@ -1843,9 +1843,12 @@ __global__ void __launch_bounds__(256) sssp_merge_kernel(int F, const int* __res
   __shared__ int s_fo[kSsspTile + 2];
   __shared__ int s_base[kSsspTile + 1];
   __shared__ float s_du[kSsspTile + 1];
+  __shared__ int s_q[kSsspTile];  // this tile's pushes (<= its edges), flushed with one global atomic
+  __shared__ int s_qn, s_qbase;
   const int tid = threadIdx.x;
   const int Ef = __ldcg(fo + F);
   const int64_t total = (int64_t)F + Ef;
+  if (tid == 0) s_qn = 0;
   for (int64_t t = blockIdx.x; t * kSsspTile < total; t += gridDim.x) {
     const int64_t d0 = t * kSsspTile, d1 = d0 + kSsspTile < total ? d0 + kSsspTile : total;
     const int i0 = __ldcg(tc + t), i1 = __ldcg(tc + t + 1);
@@ -1888,11 +1891,35 @@ __global__ void __launch_bounds__(256) sssp_merge_kernel(int F, const int* __res
         cv[e] = ev[e] >= 0 ? __ldg(col + ev[e]) : 0;
         wv[e] = ev[e] >= 0 ? __ldg(w + ev[e]) : 0.f;
       }
+      // relaxation: the stamps are read up front so that a vertex already pushed this round skips the
+      // exchange; the atomicExch still decides, so every vertex is pushed at most once per round (the
+      // frontier arrays hold n entries); pushes go to the tile's shared queue
+      int sv[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e)
-        if (ev[e] >= 0) sssp_relax(cv[e], dv[e] + wv[e], dist, stamp, round, q_out, n_out);
+      for (int e = 0; e < 8; ++e) sv[e] = ev[e] >= 0 ? __ldcg(stamp + cv[e]) : round;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        if (ev[e] < 0) continue;
+        const int v = cv[e];
+        const float nd = dv[e] + wv[e];
+        if (__float_as_int(nd) < __ldcg(reinterpret_cast<const int*>(dist) + v)) {
+          const int old = atomicMin(reinterpret_cast<int*>(dist) + v, __float_as_int(nd));
+          if (__float_as_int(nd) < old && sv[e] != round && atomicExch(stamp + v, round) != round)
+            s_q[atomicAdd(&s_qn, 1)] = v;
+        }
+      }
     }
     __syncthreads();
+    // flush the tile's pushes: one global reservation, coalesced stores
+    const int qn = s_qn;
+    if (qn > 0) {
+      if (tid == 0) s_qbase = atomicAdd(n_out, qn);
+      __syncthreads();
+      const int qb = s_qbase;
+      for (int q = tid; q < qn; q += 256) q_out[qb + q] = s_q[q];
+    }
+    __syncthreads();
+    if (tid == 0) s_qn = 0;
   }
 }
 
