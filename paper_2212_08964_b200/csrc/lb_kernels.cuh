@@ -1064,6 +1064,10 @@ __global__ void __launch_bounds__(NT, MINB) merge_wide_kernel(PipeArgs a) {
 // warp-uniform register, so there is no CTA barrier in the main loop and one warp segmented scan
 // per 256 nonzeros.  The row pass of tile t+1 runs at the end of tile t from prefetched offsets
 // and marks each row's last nonzero in a per-warp shared buffer.
+#ifndef LB_PRED_TAIL
+#define LB_PRED_TAIL 1  // stream_reduce_round: predicated first-row store and tail clear, no branches
+                        // (C3 291.5 -> 294.5 GNZ/s, C4 253.1 -> 255.5; 0 = the branchy form)
+#endif
 #ifndef LB_STEP_SYNC
 #define LB_STEP_SYNC 0  // merge_stream_kernel: 1 = __syncwarp after every round; 0 = only after a tile's row pass
                         // (lanes touch only their own tail[] entries inside a tile): C3 286.7 -> 291.4 GNZ/s
@@ -1290,6 +1294,21 @@ __device__ __forceinline__ void stream_reduce_round(const PipeArgs& a, int4 cT, 
   }
   const float lval = __shfl_up_sync(kFull, v, 1);
   const float agg_v = __shfl_sync(kFull, v, 31);
+#if LB_PRED_TAIL
+  {  // branch-free: predicated store of the first row end, predicated clear of the lane's tail entries
+    const bool lf = (B & ((1u << lane) - 1u)) != 0u;  // a row ended in an earlier lane
+    const float carry_in = lane == 0 ? rc : (lf ? lval : rc + lval);
+    if (!(LB_ABL & 1) || (LB_ABL & 4)) st_cs_if(a.y + (i0 - 1) + (int)first_rid, carry_in + first_val, first_rid != 0u);
+    if (!(LB_ABL & 4)) {
+      const unsigned ta = (unsigned)__cvta_generic_to_shared(&tail[256 * k + 8 * lane]);
+      asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q st.shared.v4.u32 [%0], {0, 0, 0, 0};\n\t}"
+                   :: "r"(ta), "r"(any) : "memory");
+      if (sizeof(TailT) == 4)  // 32-bit row ids: 8 entries are 32 bytes
+        asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\t@q st.shared.v4.u32 [%0], {0, 0, 0, 0};\n\t}"
+                     :: "r"(ta + 16u), "r"(any) : "memory");
+    }
+  }
+#else
   if (first_rid != 0u) {
     const bool lf = (B & ((1u << lane) - 1u)) != 0u;  // a row ended in an earlier lane
     const float carry_in = lane == 0 ? rc : (lf ? lval : rc + lval);
@@ -1297,6 +1316,7 @@ __device__ __forceinline__ void stream_reduce_round(const PipeArgs& a, int4 cT, 
     if (!(LB_ABL & 1) || (LB_ABL & 4)) put_y<false>(a, row, carry_in + first_val);
   }
   if (any && !(LB_ABL & 4)) tail_clear8(&tail[256 * k + 8 * lane]);
+#endif
   rc = B ? agg_v : rc + agg_v;
 }
 
