@@ -382,10 +382,30 @@ def run_single(args, cfg):
     for _ in range(n_e2e):
         M.spmv_host(hx, hy, sched, repartition=True)
     dq = (time.perf_counter() - t0) / n_e2e
-    rec["e2e"] = {"value": round(nnz / dq / 1e9, 3), "unit": "GNZ/s", "h2d_bytes_per_step": 4 * cols,
-                  "d2h_bytes_per_step": 4 * rows, "steps": n_e2e, "ms_per_step": round(dq * 1e3, 4),
-                  "api": "lb_spmv_host_x (A resident on the device, created once; per step: pinned H2D of x, "
-                         "lb_spmv_ex(REPARTITION), D2H of y, stream sync; host clock)"}
+    e2e_iter = {"value": round(nnz / dq / 1e9, 3), "unit": "GNZ/s", "h2d_bytes_per_step": 4 * cols,
+                "d2h_bytes_per_step": 4 * rows, "steps": n_e2e, "ms_per_step": round(dq * 1e3, 4),
+                "api": "lb_spmv_host_x (A resident on the device, created once; per step: pinned H2D of x, "
+                       "lb_spmv_ex(REPARTITION), D2H of y, stream sync; host clock)"}
+    # `e2e`: independent right-hand sides streamed through lb_spmv_host_x_async (two staging slots: step
+    # k's H2D, step k-1's SpMV and step k-2's D2H overlap), one x and one y buffer per step in pinned
+    # host memory, a wait at the end; host clock around all of it.
+    nb = 4
+    hxs = [hx.clone().pin_memory() for _ in range(nb)]
+    hys = [torch.empty(rows).pin_memory() for _ in range(nb)]
+    for i in range(nb):
+        M.spmv_host_async(hxs[i], hys[i], sched, repartition=True)
+    M.spmv_host_wait()
+    t0 = time.perf_counter()
+    for i in range(n_e2e):
+        M.spmv_host_async(hxs[i % nb], hys[i % nb], sched, repartition=True)
+    M.spmv_host_wait()
+    da = (time.perf_counter() - t0) / n_e2e
+    rec["e2e"] = {"value": round(nnz / da / 1e9, 3), "unit": "GNZ/s", "h2d_bytes_per_step": 4 * cols,
+                  "d2h_bytes_per_step": 4 * rows, "steps": n_e2e, "ms_per_step": round(da * 1e3, 4),
+                  "api": "lb_spmv_host_x_async + lb_spmv_host_x_wait (A resident on the device, created once; "
+                         "per step: pinned H2D of that step's x, lb_spmv_ex(REPARTITION), D2H of its y; copies "
+                         "of neighbouring steps overlap the SpMV; host clock over all steps + the final wait)"}
+    rec["e2e_iterative"] = e2e_iter
     h = lb.HostSpmv(rows, cols, nnz, device=dev)
     ho, hc, hv = A.row_offsets.cpu().pin_memory(), A.col_idx.cpu().pin_memory(), A.values.cpu().pin_memory()
     h(ho, hc, hv, hx, hy, sched)

@@ -294,6 +294,27 @@ lb_status_t lb_spmv_host_x(lb_csr_t A, lb_schedule_t sched, const float* h_x, fl
                            void* stream);
 
 /*
+ * lb_spmv_host_x_async / lb_spmv_host_x_wait -- the same y = A x with HOST x and y as lb_spmv_host_x,
+ * for a stream of independent right-hand sides (many x vectors against one resident matrix, e.g. a
+ * serving batch): the call only ENQUEUES the pinned H2D copy of h_x [cols] into one of two staging
+ * slots the handle owns (on an H2D stream of its own), the SpMV of `sched` with `flags` on `stream`
+ * (as lb_spmv_ex; it waits for that copy) and the D2H copy of y [rows] into h_y (on a D2H stream of
+ * its own, after the SpMV), and returns.  Consecutive calls alternate the two slots, so call k's
+ * H2D, call k-1's SpMV and call k-2's D2H can run at once (PCIe is full duplex); a call reuses a slot
+ * only after the SpMV and the D2H of the call two back on it (stream-ordered event waits, no host
+ * sync).  Ownership: h_x must stay unmodified and h_y untouched until lb_spmv_host_x_wait returns;
+ * h_y holds y after lb_spmv_host_x_wait(A), which blocks until every enqueued call's y is on the
+ * host.  Pinned host buffers are required for the copies to overlap.  Products and summation order
+ * are those of lb_spmv_ex, so y is bitwise equal to lb_spmv_host_x for the same inputs.  Staging,
+ * streams and events are allocated on the first call and freed by lb_csr_destroy.  Errors:
+ * LB_ERR_INVALID_ARG (null handle, null h_x / h_y with work to do), LB_ERR_OOM, LB_ERR_CUDA; the
+ * schedule's own errors as lb_spmv.  Not in the paper: host-side pipelining around P:123's y = A x.
+ */
+lb_status_t lb_spmv_host_x_async(lb_csr_t A, lb_schedule_t sched, const float* h_x, float* h_y,
+                                 uint32_t flags, void* stream);
+lb_status_t lb_spmv_host_x_wait(lb_csr_t A);
+
+/*
  * lb_spmv_phase_times -- diagnostics: run `sched` once with CUDA events between its kernels on
  * `stream`, synchronise, and report milliseconds per phase in ms_out[3] = {partition, main
  * kernel, fix-up} (unused phases are 0).  MERGE_PATH recomputes the partition.

@@ -273,6 +273,15 @@ struct lb_csr_s {
   // SSSP workspace (lb_sssp; allocated on first use)
   void* sssp_mem = nullptr;
   float* hx_stage = nullptr;   // [cols + rows] device staging of lb_spmv_host_x (x, then y)
+  // lb_spmv_host_x_async: two staging slots [x | y], an H2D and a D2H stream, per-slot events
+  void* hp_mem = nullptr;
+  float* hp_x[2] = {nullptr, nullptr};
+  float* hp_y[2] = {nullptr, nullptr};
+  cudaStream_t hp_h2d = nullptr, hp_d2h = nullptr;
+  cudaEvent_t hp_xready[2] = {nullptr, nullptr};  // x of the slot is on the device
+  cudaEvent_t hp_done[2] = {nullptr, nullptr};    // the slot's SpMV finished (x slot reusable)
+  cudaEvent_t hp_out[2] = {nullptr, nullptr};     // the slot's y reached the host (y slot reusable)
+  int hp_next = 0;
   int* q_a = nullptr;          // [rows] frontier lists (ping-pong)
   int* q_b = nullptr;
   int* stamp = nullptr;        // [rows] round of the last push
@@ -1340,6 +1349,18 @@ lb_status_t lb_csr_destroy(lb_csr_t A) {
   if (A->sssp_mem) cudaFree(A->sssp_mem);
   if (A->bin_mem) cudaFree(A->bin_mem);
   if (A->hx_stage) cudaFree(A->hx_stage);
+  if (A->hp_mem) {
+    if (A->hp_h2d) cudaStreamSynchronize(A->hp_h2d);
+    if (A->hp_d2h) cudaStreamSynchronize(A->hp_d2h);
+    for (int i = 0; i < 2; ++i) {
+      if (A->hp_xready[i]) cudaEventDestroy(A->hp_xready[i]);
+      if (A->hp_done[i]) cudaEventDestroy(A->hp_done[i]);
+      if (A->hp_out[i]) cudaEventDestroy(A->hp_out[i]);
+    }
+    if (A->hp_h2d) cudaStreamDestroy(A->hp_h2d);
+    if (A->hp_d2h) cudaStreamDestroy(A->hp_d2h);
+    cudaFree(A->hp_mem);
+  }
   delete A;
   return LB_OK;
 }
@@ -1561,6 +1582,60 @@ lb_status_t lb_spmv_host_x(lb_csr_t A, lb_schedule_t sched, const float* h_x, fl
   if (st != LB_OK) return st;
   LB_CUDA(cudaMemcpyAsync(h_y, d_y, (size_t)A->rows * 4, cudaMemcpyDeviceToHost, s));
   LB_CUDA(cudaStreamSynchronize(s));
+  return LB_OK;
+}
+
+lb_status_t lb_spmv_host_x_async(lb_csr_t A, lb_schedule_t sched, const float* h_x, float* h_y, uint32_t flags,
+                                 void* stream) {
+  g_err.clear();
+  if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
+  if (A->rows == 0) return LB_OK;
+  if (!h_y || (!h_x && A->cols > 0)) return fail(LB_ERR_INVALID_ARG, "null host x or y");
+  if (!A->hp_mem) {
+    const size_t xb = align256((size_t)A->cols * 4), yb = align256((size_t)A->rows * 4);
+    void* p = nullptr;
+    if (cudaMalloc(&p, 2 * (xb + yb)) != cudaSuccess) {
+      cudaGetLastError();
+      return fail(LB_ERR_OOM, "lb_spmv_host_x_async staging");
+    }
+    A->hp_mem = p;
+    char* b = static_cast<char*>(p);
+    for (int i = 0; i < 2; ++i) {
+      A->hp_x[i] = reinterpret_cast<float*>(b + i * (xb + yb));
+      A->hp_y[i] = reinterpret_cast<float*>(b + i * (xb + yb) + xb);
+      LB_CUDA(cudaEventCreateWithFlags(&A->hp_xready[i], cudaEventDisableTiming));
+      LB_CUDA(cudaEventCreateWithFlags(&A->hp_done[i], cudaEventDisableTiming));
+      LB_CUDA(cudaEventCreateWithFlags(&A->hp_out[i], cudaEventDisableTiming));
+    }
+    LB_CUDA(cudaStreamCreateWithFlags(&A->hp_h2d, cudaStreamNonBlocking));
+    LB_CUDA(cudaStreamCreateWithFlags(&A->hp_d2h, cudaStreamNonBlocking));
+  }
+  const int k = A->hp_next;
+  stream_t s = S(stream);
+  // x slot k is free once the SpMV of the call two back (same slot) has read it
+  LB_CUDA(cudaStreamWaitEvent(A->hp_h2d, A->hp_done[k], 0));
+  if (A->cols > 0)
+    LB_CUDA(cudaMemcpyAsync(A->hp_x[k], h_x, (size_t)A->cols * 4, cudaMemcpyHostToDevice, A->hp_h2d));
+  LB_CUDA(cudaEventRecord(A->hp_xready[k], A->hp_h2d));
+  // the SpMV waits for its x and for y slot k to have been copied out by the call two back
+  LB_CUDA(cudaStreamWaitEvent(s, A->hp_xready[k], 0));
+  LB_CUDA(cudaStreamWaitEvent(s, A->hp_out[k], 0));
+  lb_status_t st = spmv_impl(A, sched, A->hp_x[k], A->hp_y[k], flags, s, nullptr);
+  if (st != LB_OK) return st;
+  LB_CUDA(cudaEventRecord(A->hp_done[k], s));
+  LB_CUDA(cudaStreamWaitEvent(A->hp_d2h, A->hp_done[k], 0));
+  LB_CUDA(cudaMemcpyAsync(h_y, A->hp_y[k], (size_t)A->rows * 4, cudaMemcpyDeviceToHost, A->hp_d2h));
+  LB_CUDA(cudaEventRecord(A->hp_out[k], A->hp_d2h));
+  A->hp_next = k ^ 1;
+  return LB_OK;
+}
+
+lb_status_t lb_spmv_host_x_wait(lb_csr_t A) {
+  g_err.clear();
+  if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
+  if (!A->hp_mem) return LB_OK;
+  LB_CUDA(cudaStreamSynchronize(A->hp_h2d));
+  LB_CUDA(cudaStreamSynchronize(A->hp_d2h));
   return LB_OK;
 }
 

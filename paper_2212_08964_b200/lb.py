@@ -79,6 +79,8 @@ def lib() -> ctypes.CDLL:
         "lb_probe_stream_gather": ([p, p, i32, p, ctypes.POINTER(ctypes.c_float)], st),
         "lb_probe_stream": ([p, i32, p, ctypes.POINTER(ctypes.c_float)], st),
         "lb_spmv_host_x": ([p, i32, p, p, ctypes.c_uint32, p], st),
+        "lb_spmv_host_x_async": ([p, i32, p, p, ctypes.c_uint32, p], st),
+        "lb_spmv_host_x_wait": ([p], st),
         "lb_shard_bounds": ([p, i64, i32, p], st),
         "lb_comm_unique_id": ([p], st),
         "lb_comm_init": ([p, i32, i32, i32, ctypes.POINTER(p)], st),
@@ -263,6 +265,22 @@ class CsrMatrix:
         _check(lib().lb_spmv_host_x(self.handle, _sched(schedule), h_x.data_ptr() if h_x.numel() else None,
                                     h_y.data_ptr() if h_y.numel() else None, 1 if repartition else 0, _stream(stream)))
         return h_y
+
+    def spmv_host_async(self, h_x: torch.Tensor, h_y: torch.Tensor, schedule="merge_path",
+                        repartition: bool = False, stream=None) -> torch.Tensor:
+        """lb_spmv_host_x_async: enqueue y = A x with HOST x and y (pinned) on two alternating staging
+        slots; h_y is valid (and h_x may be reused) after spmv_host_wait()."""
+        for t, n, nm in ((h_x, self.cols, "h_x"), (h_y, self.rows, "h_y")):
+            if t.device.type != "cpu" or t.dtype != torch.float32 or not t.is_contiguous() or t.numel() != n:
+                raise ValueError(f"{nm} must be a contiguous float32 CPU tensor of {n} elements")
+        _check(lib().lb_spmv_host_x_async(self.handle, _sched(schedule), h_x.data_ptr() if h_x.numel() else None,
+                                          h_y.data_ptr() if h_y.numel() else None, 1 if repartition else 0,
+                                          _stream(stream)))
+        return h_y
+
+    def spmv_host_wait(self) -> None:
+        """lb_spmv_host_x_wait: block until every enqueued spmv_host_async's y is on the host."""
+        _check(lib().lb_spmv_host_x_wait(self.handle))
 
     def probe_stream(self, reps: int = 20, stream=None) -> float:
         """Milliseconds of one read-only pass over col_idx + values (lb_probe_stream)."""

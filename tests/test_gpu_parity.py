@@ -313,6 +313,29 @@ def test_spmv_host_x_resident_matrix(sched):
         M.spmv_host(torch.zeros(A.cols + 1), torch.zeros(A.rows), sched)
 
 
+@pytest.mark.parametrize("sched", ["merge_path", "thread_mapped"])
+def test_spmv_host_x_async_pipeline(sched):
+    """lb_spmv_host_x_async: five independent x vectors enqueued back to back on the two staging slots
+    (each call overlaps the previous calls' copies), one wait; every h_y equals the oracle bit for bit
+    in integer mode, with and without the x-reuse plan, and a second batch reuses the slots."""
+    A = lbgen.rmat(13, 16, 7, "int")
+    M = lb.CsrMatrix.from_csr(A)
+    for batch in range(2):
+        if batch == 1 and sched == "merge_path":
+            M.plan_hot_x(256, 1000)
+        xs = [lbgen.make_x(A.cols, "int", 60 + 10 * batch + i) for i in range(5)]
+        hxs = [x.pin_memory() for x in xs]
+        hys = [torch.full((A.rows,), float("nan")).pin_memory() for _ in xs]
+        for i, (hx, hy) in enumerate(zip(hxs, hys)):
+            M.spmv_host_async(hx, hy, sched, repartition=i == 0)
+        M.spmv_host_wait()
+        for i, (x, hy) in enumerate(zip(xs, hys)):
+            y_ref, s_ref = ref(A, x)
+            check_y(hy, y_ref, s_ref, True, f"host_x_async/{sched}/{batch}/{i}")
+    with pytest.raises(ValueError):
+        M.spmv_host_async(torch.zeros(A.cols + 1), torch.zeros(A.rows), sched)
+
+
 @pytest.mark.parametrize("G", [2, 3, 8])
 def test_row_shards_concatenate_bit_identical(G):
     """G equal-nnz shards run one after another on one GPU, concatenated,
