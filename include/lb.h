@@ -210,7 +210,7 @@ lb_status_t lb_spmm(lb_csr_t A, int64_t n, const float* d_X, int64_t ldx, float*
  * evict_last policy; cold x reads use evict_first).  Products and summation order are unchanged:
  * y is bitwise identical to the call without a plan.  Other schedules ignore the plan.
  *  slots          0 = default (16384: 64 KB of shared memory per SM); 1 .. 45056; < 0 drops the plan.
- *  warm_cols      0 = no warm tier; -1 = auto (a 40 MB budget when x (4*cols bytes) is larger
+ *  warm_cols      0 = no warm tier; -1 = auto (a 48 MB budget when x (4*cols bytes) is larger
  *                 than the L2, else none); > 0 = budget in columns.
  *  hot_cols_out   (optional) number of planned hot columns (0: no plan was kept).
  *  hot_nnz_out    (optional) number of stored entries in hot columns.

@@ -553,7 +553,7 @@ lb_status_t launch_nz_tiles(lb_csr_s* A, const float* x, float* y, stream_t s) {
 constexpr int kHotSlotsDefault = 16384;  // 64 KB of shared memory per SM (best measured on C3)
 constexpr int kHotSlotsMax = 45056;      // 176 KB
 constexpr int kHotDynMax = kHotSlotsMax * 4;
-constexpr int64_t kWarmDefaultBytes = 40ll << 20;  // warm tier budget when x exceeds the L2
+constexpr int64_t kWarmDefaultBytes = 48ll << 20;  // warm tier budget when x exceeds the L2
 
 // Peer targets of the fused multi-GPU epilogue (lb_spmv_peers / lb_spmv_multi_fused): the other ranks'
 // y, already offset to this rank's first row.

@@ -130,7 +130,7 @@ def test_plan_full_size(cfg):
     # on the device by decoding it through the tables
     deg = torch.bincount(A.col_idx.long(), minlength=A.cols).cpu().numpy()
     sc = hot_slot_table_by_sort(deg, 16384)  # library default slot budget
-    warm_budget = (40 << 20) // 4 if 4 * A.cols > torch.cuda.get_device_properties(0).L2_cache_size else 0
+    warm_budget = (48 << 20) // 4 if 4 * A.cols > torch.cuda.get_device_properties(0).L2_cache_size else 0
     wc = warm_table_by_levels(deg, sc, 16384, warm_budget)
     assert n == sc.size and hn == int(deg[sc].sum())
     assert info["warm_cols"] == wc.size and info["warm_nnz"] == int(deg[wc].sum())
