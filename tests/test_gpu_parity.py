@@ -336,6 +336,28 @@ def test_spmv_host_x_async_pipeline(sched):
         M.spmv_host_async(torch.zeros(A.cols + 1), torch.zeros(A.rows), sched)
 
 
+def test_spmv_host_x_async_edge_cases():
+    """lb_spmv_host_x_async on degenerate shapes: no nonzeros (y = +0), one giant row, pageable host
+    buffers, an odd number of calls (slot 0 used twice), and rows == 0 (no-op; wait returns)."""
+    for name, A in {"no_nnz": _csr([0] * 5001, 3), "one_giant_row": _csr([0, 200_003], 1),
+                    "empty_rows_between": _csr([0, 1, 1, 1, 5, 5, 9], 1)}.items():
+        M = lb.CsrMatrix.from_csr(A)
+        hys = []
+        for i in range(3):
+            x = torch.full((A.cols,), float(i + 1))
+            hy = torch.full((A.rows,), float("nan"))
+            M.spmv_host_async(x, hy, "merge_path")
+            hys.append((x, hy))
+        M.spmv_host_wait()
+        for x, hy in hys:
+            y_ref, s_ref = ref(A, x)
+            check_y(hy, y_ref, s_ref, True, f"host_x_async/{name}")
+    M = lb.CsrMatrix(0, 0, torch.zeros(1, dtype=torch.int32, device="cuda"),
+                     torch.zeros(0, dtype=torch.int32, device="cuda"), torch.zeros(0, device="cuda"))
+    M.spmv_host_async(torch.zeros(0), torch.zeros(0))
+    M.spmv_host_wait()
+
+
 @pytest.mark.parametrize("G", [2, 3, 8])
 def test_row_shards_concatenate_bit_identical(G):
     """G equal-nnz shards run one after another on one GPU, concatenated,
