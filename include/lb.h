@@ -211,13 +211,18 @@ lb_status_t lb_spmm(lb_csr_t A, int64_t n, const float* d_X, int64_t ldx, float*
  * y is bitwise identical to the call without a plan.  Other schedules ignore the plan.
  *  slots          0 = default (16384: 64 KB of shared memory per SM); 1 .. 45056; < 0 drops the plan.
  *  warm_cols      0 = no warm tier; -1 = auto (a 48 MB budget when x (4*cols bytes) is larger
- *                 than the L2, else none); > 0 = budget in columns.
+ *                 than the L2, else none); > 0 = budget in columns; -2 = compact x: EVERY
+ *                 referenced non-hot column is warm (numbered in ascending column order), its entry
+ *                 holds the warm index itself, each call builds x_warm by a mask-driven compaction
+ *                 sweep over x (fused into the partition launch) and the tile kernel gathers from
+ *                 x_warm as its x -- the gathered footprint shrinks from all of x to the referenced
+ *                 columns.  Falls back to no warm tier when the hot set is not full.
  *  hot_cols_out   (optional) number of planned hot columns (0: no plan was kept).
  *  hot_nnz_out    (optional) number of stored entries in hot columns.
  * Cost: device memory 4*nnz + 8*(hot + warm) + 4*cols (temporary); a degree histogram, a few
  * selection passes and a remap of col_idx; synchronises `stream`.  The caller's arrays are not
  * modified.  Errors: LB_ERR_UNSUPPORTED if col_idx/values are not 32-byte aligned; LB_ERR_OOM;
- * LB_ERR_INVALID_ARG for slots > 45056 or warm_cols < -1.  Re-plan (or drop the plan) after
+ * LB_ERR_INVALID_ARG for slots > 45056 or warm_cols < -2.  Re-plan (or drop the plan) after
  * modifying col_idx.
  */
 lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, int64_t warm_cols, void* stream, int32_t* hot_cols_out,

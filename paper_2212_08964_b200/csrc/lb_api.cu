@@ -270,6 +270,10 @@ struct lb_csr_s {
   float* x_warm = nullptr;      // [warm_n] x of the warm columns, gathered every call
   int warm_n = 0;
   int64_t warm_nnz = 0;
+  bool compact = false;
+  unsigned* wmask = nullptr;    // compact: [ceil(cols/32)] bit c = column c is warm
+  int* wbase = nullptr;         // compact: [ceil(cols/32)] warm index of the word's first warm column         // warm_cols = -2: every referenced non-hot column is warm and the tile
+                                // kernel gathers from the dense x_warm as its x (TIER 1 path)
   // SSSP workspace (lb_sssp; allocated on first use)
   void* sssp_mem = nullptr;
   float* hx_stage = nullptr;   // [cols + rows] device staging of lb_spmv_host_x (x, then y)
@@ -553,6 +557,7 @@ lb_status_t launch_nz_tiles(lb_csr_s* A, const float* x, float* y, stream_t s) {
 constexpr int kHotSlotsDefault = 16384;  // 64 KB of shared memory per SM (best measured on C3)
 constexpr int kHotSlotsMax = 45056;      // 176 KB
 constexpr int kHotDynMax = kHotSlotsMax * 4;
+constexpr int64_t kWarmCompact = -2;  // lb_csr_plan_hot_x warm_cols: compact x (all referenced columns)
 constexpr int64_t kWarmDefaultBytes = 48ll << 20;  // warm tier budget when x exceeds the L2
 
 // Peer targets of the fused multi-GPU epilogue (lb_spmv_peers / lb_spmv_multi_fused): the other ranks'
@@ -633,6 +638,7 @@ lb_status_t hot_launch_t(lb_csr_s* A, const float* x, float* y, stream_t s, cons
 }
 
 lb_status_t hot_launch(lb_csr_s* A, const float* x, float* y, stream_t s, const PeerArgs* pa = nullptr) {
+  if (A->compact) return hot_launch_t<1>(A, A->x_warm, y, s, pa);
   return A->warm_n > 0 ? hot_launch_t<2>(A, x, y, s, pa) : hot_launch_t<1>(A, x, y, s, pa);
 }
 
@@ -699,10 +705,13 @@ lb_status_t probe_launch(lb_csr_s* A, const float* x, stream_t s) {
 // partition (T >= 0) and/or the x_hot gather in one launch
 lb_status_t launch_partition_xhot(const lb_csr_s* A, int64_t L, bool partition, const float* x, stream_t s) {
   const int64_t T = partition ? num_tiles(A->rows, A->nnz, L) : -1;
-  const int64_t n = T + 1 + A->hot_n + A->warm_n;
+  const int warm_idx = A->compact ? 0 : A->warm_n;               // warm gather by index
+  const int64_t nquad = A->compact ? (A->cols + 3) / 4 : 0;      // or by mask (compact plan)
+  const int64_t n = T + 1 + A->hot_n + warm_idx + nquad;
   const int grid = (int)std::max<int64_t>(1, (n + kNT - 1) / kNT);
   lbk::partition_xhot_kernel<<<grid, kNT, 0, s>>>((int)A->rows, (int)A->nnz, A->off, L, T, A->coords, A->hot_cols,
-                                                   A->hot_n, A->warm_cols, A->warm_n, x, A->x_hot, A->x_warm);
+                                                   A->hot_n, A->warm_cols, warm_idx, x, A->x_hot, A->x_warm,
+                                                   A->wmask, A->wbase, nquad);
   LB_LAUNCHED();
   return LB_OK;
 }
@@ -714,6 +723,9 @@ void drop_plan(lb_csr_s* A) {
   A->x_hot = A->x_warm = nullptr;
   A->hot_n = A->hot_n4 = A->warm_n = 0;
   A->hot_nnz = A->warm_nnz = 0;
+  A->compact = false;
+  A->wmask = nullptr;
+  A->wbase = nullptr;
 }
 
 // Degree level of the K-th most referenced column (candidates: deg >= 2), by successive equal-width
@@ -763,6 +775,7 @@ lb_status_t find_level(lb_csr_s* A, const int* deg, int* bins, int64_t K, stream
 // Builds the plan (see lb.h lb_csr_plan_hot_x).  Synchronises `s` a few times (setup call).
 lb_status_t build_plan(lb_csr_s* A, int slots, int64_t warm, stream_t s) {
   drop_plan(A);
+  const bool compact = warm == kWarmCompact;
   const int cols = (int)A->cols;
   const int64_t nnz = A->nnz;
   const int nblk = (int)((A->cols + lbk::kHotChunk - 1) / lbk::kHotChunk);
@@ -791,7 +804,10 @@ lb_status_t build_plan(lb_csr_s* A, int slots, int64_t warm, stream_t s) {
   if (l1.found) { t1_hi = (int)(l1.tau + 1); t1_tie = (int)l1.tau; b1 = (int)(slots - l1.above); }
   // warm tier: whole degree levels below the hot set, at most `warm` more columns
   int t2 = INT_MAX, warm_on = 0;
-  if (warm > 0 && l1.found) {
+  if (compact && l1.found) {
+    t2 = 1;  // every referenced column below the hot set
+    warm_on = 1;
+  } else if (warm > 0 && l1.found) {
     Level l2;
     if ((st = find_level(A, deg, bins, (int64_t)slots + warm, s, &l2)) != LB_OK) return st;
     const int64_t tau2 = !l2.found ? 2 : (l2.above + l2.at == (int64_t)slots + warm ? l2.tau : l2.tau + 1);
@@ -811,8 +827,10 @@ lb_status_t build_plan(lb_csr_s* A, int slots, int64_t warm, stream_t s) {
   if (hot_n == 0) return LB_OK;  // nothing worth caching: no plan
 
   const int hot_n4 = (hot_n + 3) / 4;
+  const bool cmp = compact && warm_n > 0;
+  const size_t nwords = ((size_t)cols + 31) / 32;
   const size_t plan_bytes = align256((size_t)nnz * 4) + align256((size_t)hot_n * 4) + align256((size_t)hot_n4 * 16) +
-                            2 * align256((size_t)std::max(warm_n, 1) * 4);
+                            2 * align256((size_t)std::max(warm_n, 1) * 4) + (cmp ? 2 * align256(nwords * 4) : 0);
   void* pm = nullptr;
   if (cudaMalloc(&pm, plan_bytes) != cudaSuccess) { cudaGetLastError(); return fail(LB_ERR_OOM, "plan (%zu bytes)", plan_bytes); }
   char* q = static_cast<char*>(pm);
@@ -825,13 +843,21 @@ lb_status_t build_plan(lb_csr_s* A, int slots, int64_t warm, stream_t s) {
   int32_t* warm_cols = reinterpret_cast<int32_t*>(q);
   q += align256((size_t)std::max(warm_n, 1) * 4);
   float* x_warm = reinterpret_cast<float*>(q);
+  q += align256((size_t)std::max(warm_n, 1) * 4);
+  unsigned* wmask = cmp ? reinterpret_cast<unsigned*>(q) : nullptr;
+  int* wbase = cmp ? reinterpret_cast<int*>(q + align256(nwords * 4)) : nullptr;
   LB_CUDA(cudaMemsetAsync(x_hot, 0, (size_t)hot_n4 * 16, s));
   LB_CUDA(cudaMemsetAsync(d_sums, 0, 16, s));
   lbk::plan_assign_kernel<<<nblk, 256, 0, s>>>(cols, deg, t1_hi, t1_tie, t2, n_above, b1, hot_n, blk, hot_cols,
                                                warm_cols, d_sums);
   LB_LAUNCHED();
-  lbk::plan_remap_kernel<<<sms * 8, kNT, 0, s>>>(nnz, cols, hot_n, A->col, deg, hcol);
+  lbk::plan_remap_kernel<<<sms * 8, kNT, 0, s>>>(nnz, cmp ? 0 : cols, hot_n, A->col, deg, hcol);
   LB_LAUNCHED();
+  if (cmp) {
+    LB_CUDA(cudaMemsetAsync(wmask, 0, nwords * 4, s));
+    lbk::plan_mask_kernel<<<sms * 8, kNT, 0, s>>>(warm_cols, warm_n, wmask, wbase);
+    LB_LAUNCHED();
+  }
   unsigned long long sums[2] = {0, 0};
   LB_CUDA(cudaMemcpyAsync(sums, d_sums, sizeof sums, cudaMemcpyDeviceToHost, s));
   LB_CUDA(cudaStreamSynchronize(s));
@@ -845,6 +871,9 @@ lb_status_t build_plan(lb_csr_s* A, int slots, int64_t warm, stream_t s) {
   A->warm_cols = warm_cols;
   A->x_warm = x_warm;
   A->warm_n = warm_n;
+  A->compact = cmp;
+  A->wmask = wmask;
+  A->wbase = wbase;
   A->warm_nnz = (int64_t)sums[1];
   return LB_OK;
 }
@@ -1395,10 +1424,11 @@ lb_status_t lb_probe_stream_gather(lb_csr_t A, const float* d_x, int32_t reps, v
   if (!A || !ms_out || reps < 1 || (!d_x && A->nnz > 0)) return fail(LB_ERR_INVALID_ARG, "bad probe arguments");
   if (!A->vec32) return fail(LB_ERR_UNSUPPORTED, "probe needs 32-byte aligned col_idx/values");
   stream_t s = S(stream);
-  const int tier = A->hot_n > 0 ? (A->warm_n > 0 ? 2 : 1) : 0;
+  const int tier = A->hot_n > 0 ? (A->warm_n > 0 && !A->compact ? 2 : 1) : 0;
   lb_status_t st;
   if (tier > 0 && (st = launch_partition_xhot(A, 0, false, d_x, s)) != LB_OK) return st;  // x_hot / x_warm of this x
-  auto launch = [&]() { return tier == 2 ? probe_launch<2>(A, d_x, s) : tier == 1 ? probe_launch<1>(A, d_x, s)
+  const float* xg = A->compact ? A->x_warm : d_x;
+  auto launch = [&]() { return tier == 2 ? probe_launch<2>(A, d_x, s) : tier == 1 ? probe_launch<1>(A, xg, s)
                                                                                    : probe_launch<0>(A, d_x, s); };
   if ((st = launch()) != LB_OK) return st;  // warm-up
   cudaEvent_t e0, e1;
@@ -1457,7 +1487,7 @@ lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, int64_t warm_cols, void
   } else {
     if (slots == 0) slots = kHotSlotsDefault;
     if (slots > kHotSlotsMax) return fail(LB_ERR_INVALID_ARG, "slots %d > %d", slots, kHotSlotsMax);
-    if (warm_cols < -1) return fail(LB_ERR_INVALID_ARG, "warm_cols %lld < -1", (long long)warm_cols);
+    if (warm_cols < -2) return fail(LB_ERR_INVALID_ARG, "warm_cols %lld < -2", (long long)warm_cols);
     if (!A->vec32) return fail(LB_ERR_UNSUPPORTED, "x-reuse plan needs 32-byte aligned col_idx/values");
     if (warm_cols == -1) {  // auto: only when x is larger than the L2 (measured: C5 2.2x, C3 -10%)
       int l2 = 0;

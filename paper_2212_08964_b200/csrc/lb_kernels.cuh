@@ -139,7 +139,9 @@ __global__ void partition_kernel(int rows, int nnz, const int* __restrict__ off,
 __global__ void partition_xhot_kernel(int rows, int nnz, const int* __restrict__ off, int64_t L, int64_t T,
                                       int2* __restrict__ coords, const int* __restrict__ hot_cols, int hot_n,
                                       const int* __restrict__ warm_cols, int warm_n, const float* __restrict__ x,
-                                      float* __restrict__ x_hot, float* __restrict__ x_warm) {
+                                      float* __restrict__ x_hot, float* __restrict__ x_warm,
+                                      const unsigned* __restrict__ wmask = nullptr,
+                                      const int* __restrict__ wbase = nullptr, int64_t nquad = 0) {
   asm volatile("griddepcontrol.launch_dependents;");
   const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (t <= T) {
@@ -152,7 +154,36 @@ __global__ void partition_xhot_kernel(int rows, int nnz, const int* __restrict__
     return;
   }
   const int64_t w = h - hot_n;  // warm columns ascend, so these reads sweep x in address order
-  if (w < warm_n) x_warm[w] = __ldg(x + __ldg(warm_cols + w));
+  if (w < warm_n) {
+    x_warm[w] = __ldg(x + __ldg(warm_cols + w));
+    return;
+  }
+  // compact plan: x_warm = the referenced non-hot entries of x in column order, by stream compaction
+  // with the plan's bit mask (wmask: bit c of the warm columns; wbase: warm index of the word's first
+  // one).  Thread u covers columns 4u .. 4u+3 and reads only the ones it keeps (coalesced sweep).
+  const int64_t u = w - warm_n;
+  if (u < nquad) {
+    const unsigned m = __ldg(wmask + (u >> 3));
+    const int sh = (int)(u & 7) * 4;
+    unsigned bits = (m >> sh) & 0xFu;
+    if (!bits) return;
+    int o = __ldg(wbase + (u >> 3)) + __popc(m & ((1u << sh) - 1u));
+    const float* xq = x + 4 * u;
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (bits & (1u << e)) x_warm[o++] = __ldg(xq + e);
+  }
+}
+
+// compact plan: bit mask and per-word base index of the warm columns (ascending list)
+__global__ void plan_mask_kernel(const int* __restrict__ warm_cols, int warm_n, unsigned* __restrict__ wmask,
+                                 int* __restrict__ wbase) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < warm_n; w += stride) {
+    const int c = __ldg(warm_cols + w);
+    atomicOr(wmask + (c >> 5), 1u << (c & 31));
+    if (w == 0 || (__ldg(warm_cols + w - 1) >> 5) != (c >> 5)) wbase[c >> 5] = (int)w;
+  }
 }
 
 // Nonzero-splitting partition (table; reading R19): tiles of L nonzeros, T = max(1,

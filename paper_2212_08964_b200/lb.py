@@ -320,7 +320,7 @@ class CsrMatrix:
 
     def plan_hot_x(self, slots: int = 0, warm: int = -1, stream=None) -> tuple[int, int]:
         """Build (slots >= 0; 0 = library default) or drop (slots < 0) the x-reuse plan
-        (lb_csr_plan_hot_x; warm: 0 none, -1 auto, > 0 column budget).  Returns (hot columns,
+        (lb_csr_plan_hot_x; warm: 0 none, -1 auto, > 0 column budget, -2 compact x).  Returns (hot columns,
         stored entries in them); plan_info() has the warm tier."""
         n, h = ctypes.c_int32(), ctypes.c_int64()
         _check(lib().lb_csr_plan_hot_x(self.handle, int(slots), int(warm), _stream(stream), ctypes.byref(n),
