@@ -376,16 +376,19 @@ def run_single(args, cfg):
     # same lb_spmv_ex(REPARTITION) step and copies y out (the call synchronises; host clock per step).
     # `e2e_full_upload`: lb_spmv_host -- the whole CSR + x uploaded every step (PCIe-bound).
     hx, hy = x.cpu().pin_memory(), torch.empty(rows).pin_memory()
-    M.spmv_host(hx, hy, sched, repartition=True)
+    chunked = plan is not None
+    M.spmv_host(hx, hy, sched, repartition=True, chunked=chunked)
     n_e2e = max(20, args.e2e_steps)
     t0 = time.perf_counter()
     for _ in range(n_e2e):
-        M.spmv_host(hx, hy, sched, repartition=True)
+        M.spmv_host(hx, hy, sched, repartition=True, chunked=chunked)
     dq = (time.perf_counter() - t0) / n_e2e
     e2e_iter = {"value": round(nnz / dq / 1e9, 3), "unit": "GNZ/s", "h2d_bytes_per_step": 4 * cols,
                 "d2h_bytes_per_step": 4 * rows, "steps": n_e2e, "ms_per_step": round(dq * 1e3, 4),
-                "api": "lb_spmv_host_x (A resident on the device, created once; per step: pinned H2D of x, "
-                       "lb_spmv_ex(REPARTITION), D2H of y, stream sync; host clock)"}
+                "api": "lb_spmv_host_x" + ("(REPARTITION | CHUNKED: y rows copied out per tile-range launch while "
+                                           "the next range computes)" if chunked else "(REPARTITION)")
+                       + " (A resident on the device, created once; per step: pinned H2D of x, the SpMV, D2H of "
+                         "y, stream sync; host clock)"}
     # `e2e`: independent right-hand sides streamed through lb_spmv_host_x_async (two staging slots: step
     # k's H2D, step k-1's SpMV and step k-2's D2H overlap), one x and one y buffer per step in pinned
     # host memory, a wait at the end; host clock around all of it.

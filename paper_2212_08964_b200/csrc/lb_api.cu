@@ -237,6 +237,8 @@ int pipe_variant_for(int L) {
 
 }  // namespace
 
+constexpr int kChunksMax = 8;  // LB_SPMV_CHUNKED: row chunks whose y copies overlap the next chunk
+
 struct lb_csr_s {
   int64_t rows = 0, cols = 0, nnz = 0;
   const int32_t* off = nullptr;
@@ -286,6 +288,13 @@ struct lb_csr_s {
   cudaEvent_t hp_done[2] = {nullptr, nullptr};    // the slot's SpMV finished (x slot reusable)
   cudaEvent_t hp_out[2] = {nullptr, nullptr};     // the slot's y reached the host (y slot reusable)
   int hp_next = 0;
+  // tile range of the next merge-path tile-kernel launch (LB_SPMV_CHUNKED; tr_t1 < 0: all tiles)
+  int64_t tr_t0 = 0, tr_t1 = -1;
+  // cached clean chunk boundaries for LB_SPMV_CHUNKED: tiles ch_t[0..ch_n], first rows ch_i[0..ch_n]
+  int ch_L = 0, ch_n = 0;
+  int64_t ch_t[kChunksMax + 1] = {}, ch_i[kChunksMax + 1] = {};
+  cudaStream_t ch_d2h = nullptr;
+  cudaEvent_t ch_ev[kChunksMax] = {};
   int* q_a = nullptr;          // [rows] frontier lists (ping-pong)
   int* q_b = nullptr;
   int* stamp = nullptr;        // [rows] round of the last push
@@ -590,14 +599,16 @@ lb_status_t hot_launch_wr(lb_csr_s* A, const float* x, float* y, stream_t s, con
     conf_dyn[A->device] = dyn;
   }
   constexpr int L = 256 * R - 8;
-  const int T = (int)num_tiles(A->rows, A->nnz, L);
+  const bool ranged = A->tr_t1 >= 0;  // LB_SPMV_CHUNKED: tiles [tr_t0, tr_t1) only
+  const int T = ranged ? (int)(A->tr_t1 - A->tr_t0) : (int)num_tiles(A->rows, A->nnz, L);
+  if (T <= 0) return LB_OK;
   const int warps_max = std::min(A->dev->sm_count * W, kMaxCtas);
   const int tpw = (T + warps_max - 1) / warps_max;
   const int warps = (T + tpw - 1) / tpw;
   const int grid = (warps + W - 1) / W;
   lbk::PipeArgs a;
   a.off = A->off; a.col = A->hcol; a.val = A->val; a.x = x; a.y = y;
-  a.coords = A->coords; a.rows = (int)A->rows; a.nnz = (int)A->nnz;
+  a.coords = A->coords + (ranged ? A->tr_t0 : 0); a.rows = (int)A->rows; a.nnz = (int)A->nnz;
   a.num_tiles = T; a.tiles_per_cta = tpw;
   a.carry_row = A->carry_row; a.carry_val = A->carry_val; a.ticket = A->ticket;
   a.x_hot = A->x_hot; a.hot_n4 = A->hot_n4;
@@ -1378,6 +1389,12 @@ lb_status_t lb_csr_destroy(lb_csr_t A) {
   if (A->sssp_mem) cudaFree(A->sssp_mem);
   if (A->bin_mem) cudaFree(A->bin_mem);
   if (A->hx_stage) cudaFree(A->hx_stage);
+  if (A->ch_d2h) {
+    cudaStreamSynchronize(A->ch_d2h);
+    for (auto& e : A->ch_ev)
+      if (e) cudaEventDestroy(e);
+    cudaStreamDestroy(A->ch_d2h);
+  }
   if (A->hp_mem) {
     if (A->hp_h2d) cudaStreamSynchronize(A->hp_h2d);
     if (A->hp_d2h) cudaStreamSynchronize(A->hp_d2h);
@@ -1589,6 +1606,57 @@ lb_status_t lb_spmv_phase_times(lb_csr_t A, lb_schedule_t sched, const float* d_
   return st;
 }
 
+// LB_SPMV_CHUNKED: the merge-path step with the hot plan as kChunks tile-kernel launches over tile
+// ranges that start and end on clean merge-path coordinates (no row split across a boundary, so each
+// launch's rows are final when it ends); the D2H copy of chunk k's rows overlaps chunk k+1.
+constexpr int kChunks = 4;
+lb_status_t host_x_chunked(lb_csr_s* A, const float* d_x, float* d_y, float* h_y, uint32_t flags, stream_t s) {
+  lb_status_t st;
+  const bool repart = !A->coords_valid || A->coords_kind != 0 || A->coords_L != A->L || (flags & LB_SPMV_REPARTITION);
+  if ((st = launch_partition_xhot(A, A->L, repart, d_x, s)) != LB_OK) return st;
+  if (repart) { A->coords_valid = true; A->coords_L = A->L; A->coords_kind = 0; }
+  if (!A->ch_d2h) {
+    LB_CUDA(cudaStreamCreateWithFlags(&A->ch_d2h, cudaStreamNonBlocking));
+    for (auto& e : A->ch_ev) LB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  const int64_t T = num_tiles(A->rows, A->nnz, A->L);
+  if (A->ch_L != A->L) {  // chunk boundaries of this tile length (deterministic: computed once)
+    int* d_out = nullptr;
+    if (cudaMalloc(&d_out, 2 * kChunks * sizeof(int)) != cudaSuccess) { cudaGetLastError(); return fail(LB_ERR_OOM, "chunks"); }
+    lbk::clean_tiles_kernel<<<1, 32, 0, s>>>(A->coords, A->off, T, kChunks, 4096, d_out);
+    LB_LAUNCHED();
+    int h[2 * kChunks] = {};
+    cudaError_t e1 = cudaMemcpyAsync(h, d_out, sizeof h, cudaMemcpyDeviceToHost, s);
+    cudaError_t e2 = e1 == cudaSuccess ? cudaStreamSynchronize(s) : e1;
+    cudaFree(d_out);
+    if (e2 != cudaSuccess) return fail(LB_ERR_CUDA, "chunk boundaries: %s", cudaGetErrorString(e2));
+    int n = 0;
+    A->ch_t[0] = 0; A->ch_i[0] = 0;
+    for (int k = 1; k < kChunks; ++k)
+      if (h[k] > A->ch_t[n] && h[k] < T) { ++n; A->ch_t[n] = h[k]; A->ch_i[n] = h[kChunks + k]; }
+    ++n;
+    A->ch_t[n] = T; A->ch_i[n] = A->rows;
+    A->ch_n = n;
+    A->ch_L = A->L;
+  }
+  for (int k = 0; k < A->ch_n; ++k) {
+    A->tr_t0 = A->ch_t[k];
+    A->tr_t1 = A->ch_t[k + 1];
+    st = hot_launch(A, d_x, d_y, s);
+    A->tr_t0 = 0;
+    A->tr_t1 = -1;
+    if (st != LB_OK) return st;
+    LB_CUDA(cudaEventRecord(A->ch_ev[k], s));
+    LB_CUDA(cudaStreamWaitEvent(A->ch_d2h, A->ch_ev[k], 0));
+    const int64_t r0 = A->ch_i[k], r1 = A->ch_i[k + 1];
+    if (r1 > r0)
+      LB_CUDA(cudaMemcpyAsync(h_y + r0, d_y + r0, (size_t)(r1 - r0) * 4, cudaMemcpyDeviceToHost, A->ch_d2h));
+  }
+  LB_CUDA(cudaStreamSynchronize(A->ch_d2h));
+  LB_CUDA(cudaStreamSynchronize(s));
+  return LB_OK;
+}
+
 lb_status_t lb_spmv_host_x(lb_csr_t A, lb_schedule_t sched, const float* h_x, float* h_y, uint32_t flags,
                            void* stream) {
   g_err.clear();
@@ -1608,6 +1676,8 @@ lb_status_t lb_spmv_host_x(lb_csr_t A, lb_schedule_t sched, const float* h_x, fl
   float* d_x = A->hx_stage;
   float* d_y = reinterpret_cast<float*>(reinterpret_cast<char*>(A->hx_stage) + align256((size_t)A->cols * 4));
   if (A->cols > 0) LB_CUDA(cudaMemcpyAsync(d_x, h_x, (size_t)A->cols * 4, cudaMemcpyHostToDevice, s));
+  if ((flags & LB_SPMV_CHUNKED) && sched == LB_SCHED_MERGE_PATH && hot_usable(A))
+    return host_x_chunked(A, d_x, d_y, h_y, flags, s);
   lb_status_t st = spmv_impl(A, sched, d_x, d_y, flags, s, nullptr);
   if (st != LB_OK) return st;
   LB_CUDA(cudaMemcpyAsync(h_y, d_y, (size_t)A->rows * 4, cudaMemcpyDeviceToHost, s));

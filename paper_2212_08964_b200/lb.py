@@ -23,6 +23,7 @@ SCHEDULES = {"thread_mapped": 0, "group_mapped": 1, "merge_path": 2, "block_mapp
              "nonzero_split": 5, "warp_mapped": 6, "binning": 7}
 SCHEDULE_NAMES = {v: k for k, v in SCHEDULES.items()}
 LB_SPMV_REPARTITION = 1
+LB_SPMV_CHUNKED = 2
 DEFAULT_ITEMS_PER_TILE = 1016
 TILE_LENGTHS = (504, 1016, 2040, 3064, 4088)
 
@@ -256,14 +257,16 @@ class CsrMatrix:
         return Y
 
     def spmv_host(self, h_x: torch.Tensor, h_y: torch.Tensor, schedule="merge_path", repartition: bool = False,
-                  stream=None) -> torch.Tensor:
+                  stream=None, chunked: bool = False) -> torch.Tensor:
         """lb_spmv_host_x: y = A x with x and y in HOST memory (pinned for full bandwidth); the matrix stays
-        on the device.  Returns h_y after the call has synchronised."""
+        on the device.  chunked: LB_SPMV_CHUNKED (y copied out per row chunk while the next computes).
+        Returns h_y after the call has synchronised."""
         for t, n, nm in ((h_x, self.cols, "h_x"), (h_y, self.rows, "h_y")):
             if t.device.type != "cpu" or t.dtype != torch.float32 or not t.is_contiguous() or t.numel() != n:
                 raise ValueError(f"{nm} must be a contiguous float32 CPU tensor of {n} elements")
+        flags = (LB_SPMV_REPARTITION if repartition else 0) | (LB_SPMV_CHUNKED if chunked else 0)
         _check(lib().lb_spmv_host_x(self.handle, _sched(schedule), h_x.data_ptr() if h_x.numel() else None,
-                                    h_y.data_ptr() if h_y.numel() else None, 1 if repartition else 0, _stream(stream)))
+                                    h_y.data_ptr() if h_y.numel() else None, flags, _stream(stream)))
         return h_y
 
     def spmv_host_async(self, h_x: torch.Tensor, h_y: torch.Tensor, schedule="merge_path",

@@ -336,6 +336,44 @@ def test_spmv_host_x_async_pipeline(sched):
         M.spmv_host_async(torch.zeros(A.cols + 1), torch.zeros(A.rows), sched)
 
 
+@pytest.mark.parametrize("case", ["rmat13", "rmat15_float", "giant_row", "ragged"])
+def test_spmv_host_x_chunked(case):
+    """lb_spmv_host_x(LB_SPMV_CHUNKED): the hot-plan tile kernel as up to 4 launches over tile ranges cut
+    at clean merge-path coordinates, y rows copied out per range.  Integer mode bit-exact against the
+    oracle; float mode within tolerance; a giant row with no clean cut inside it; repeated calls with
+    a new x reuse the cached cuts."""
+    if case == "rmat13":
+        A, vm = lbgen.rmat(13, 16, 21, "int"), "int"
+    elif case == "rmat15_float":
+        A, vm = lbgen.rmat(15, 16, 22, "float"), "float"
+    elif case == "giant_row":
+        A, vm = _csr([0, 3, 3, 200_003, 200_010] + [200_010 + 5 * i for i in range(1, 600)], 1), "int"
+    else:
+        A, vm = lbgen.skewed(16_384, 5, 20_000, 300_000, 23, "int"), "int"
+    M = lb.CsrMatrix.from_csr(A)
+    if M.plan_hot_x(64 if A.cols >= 64 else 1, 0)[0] == 0:
+        pytest.skip("no hot plan for this matrix")
+    for it in range(3):
+        x = lbgen.make_x(A.cols, vm, 500 + it) if A.cols > 1 else torch.full((1,), float(it + 1))
+        y_ref, s_ref = ref(A, x)
+        hy = torch.full((A.rows,), float("nan")).pin_memory()
+        M.spmv_host(x.pin_memory(), hy, "merge_path", repartition=it == 0, chunked=True)
+        check_y(hy, y_ref, s_ref, vm == "int", f"chunked/{case}/{it}")
+
+
+def test_spmv_host_x_chunked_full_size_c3():
+    """LB_SPMV_CHUNKED at the bench's configuration (C3, default plan), integer mode: the host y equals
+    the one-launch device call bit for bit (both exact)."""
+    A = lbgen.make_config("c3", "int", device="cuda")
+    x = lbgen.x_for_config("c3", A.cols, "int", device="cuda")
+    M = lb.CsrMatrix.from_csr(A)
+    M.plan_hot_x(0)
+    y = M.spmv(x, schedule="merge_path", repartition=True)
+    hy = torch.full((A.rows,), float("nan")).pin_memory()
+    M.spmv_host(x.cpu().pin_memory(), hy, "merge_path", repartition=True, chunked=True)
+    assert torch.equal(hy, y.cpu())
+
+
 def test_spmv_host_x_async_edge_cases():
     """lb_spmv_host_x_async on degenerate shapes: no nonzeros (y = +0), one giant row, pageable host
     buffers, an odd number of calls (slot 0 used twice), and rows == 0 (no-op; wait returns)."""
