@@ -269,7 +269,7 @@ lb_status_t lb_bins(lb_csr_t A, int32_t* d_ids, int64_t h_sizes[3], void* stream
 /* Flags for lb_spmv_ex. */
 #define LB_SPMV_REPARTITION 1u /* MERGE_PATH: recompute the partition inside this call */
 #define LB_SPMV_CHUNKED 2u     /* lb_spmv_host_x, MERGE_PATH with an x-reuse plan: run the tile kernel as
-                                  up to 4 launches over tile ranges cut at clean merge-path coordinates
+                                  up to 8 launches over tile ranges cut at clean merge-path coordinates
                                   (no row split across a cut) and copy each range's y rows to the host
                                   while the next range computes.  Same products; a row's summation
                                   order can differ from the one-launch call (carries per launch), so

@@ -1609,7 +1609,7 @@ lb_status_t lb_spmv_phase_times(lb_csr_t A, lb_schedule_t sched, const float* d_
 // LB_SPMV_CHUNKED: the merge-path step with the hot plan as kChunks tile-kernel launches over tile
 // ranges that start and end on clean merge-path coordinates (no row split across a boundary, so each
 // launch's rows are final when it ends); the D2H copy of chunk k's rows overlaps chunk k+1.
-constexpr int kChunks = 4;
+constexpr int kChunks = 8;
 lb_status_t host_x_chunked(lb_csr_s* A, const float* d_x, float* d_y, float* h_y, uint32_t flags, stream_t s) {
   lb_status_t st;
   const bool repart = !A->coords_valid || A->coords_kind != 0 || A->coords_L != A->L || (flags & LB_SPMV_REPARTITION);
