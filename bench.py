@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=10.0, help="budget for the cpu_baseline sample")
     ap.add_argument("--multi", action="store_true", help="use the multi-GPU step even at world size 1 (testing)")
+    ap.add_argument("--overlap", action="store_true",
+                    help="multi-GPU step with LB_SPMV_CHUNKED: each chunk's rows all-gathered while the next computes")
     ap.add_argument("--fused", action="store_true",
                     help="multi-GPU step with the all-gather fused into the tile kernel (lb_spmv_multi_fused)")
     ap.add_argument("--hot-slots", type=int, default=0,
@@ -463,7 +465,7 @@ def run_multi(args, cfg):
         if peer is not None:
             comm.spmv_multi_fused(M, b, x, peer, args.schedule, repartition=True)
         else:
-            comm.spmv_multi(M, b, x, y, args.schedule, repartition=True)
+            comm.spmv_multi(M, b, x, y, args.schedule, repartition=True, chunked=args.overlap)
 
     def timed(fn, n):
         dist.barrier()
@@ -592,6 +594,9 @@ def run_multi(args, cfg):
                        "schedule": args.schedule, "parallelism": f"row shards x{world} (equal nnz), NCCL all-gather of y",
                        "step": ("lb_spmv_multi_fused(REPARTITION): shard partition + SpMV whose epilogue stores y "
                                 "into every rank's buffer over NVLink + barrier") if args.fused else
+                               ("lb_spmv_multi_ex(REPARTITION | CHUNKED): shard partition + SpMV as tile-range launches, "
+                                "each chunk's rows all-gathered (NCCL broadcast group) while the next computes")
+                               if args.overlap else
                                "lb_spmv_multi_ex(REPARTITION): shard partition + SpMV + all-gather(v) of y",
                        "l2": "inputs larger than L2; no flush"},
             "plan": plan,

@@ -273,7 +273,14 @@ lb_status_t lb_bins(lb_csr_t A, int32_t* d_ids, int64_t h_sizes[3], void* stream
                                   (no row split across a cut) and copy each range's y rows to the host
                                   while the next range computes.  Same products; a row's summation
                                   order can differ from the one-launch call (carries per launch), so
-                                  y is within tolerance of it, bit-exact in integer mode. */
+                                  y is within tolerance of it, bit-exact in integer mode.
+                                  lb_spmv_multi_ex: the same cuts on every rank's shard; once chunk c is
+                                  done, an NCCL group of broadcasts sends every rank's chunk-c rows (on an
+                                  exchange stream of the handle) while chunk c+1 computes.  Collective:
+                                  all ranks pass it, with the same tile length, and build or drop their
+                                  plans together (the cut table is exchanged on the first such call and
+                                  after a plan change).  A rank without a plan sends its rows as one
+                                  chunk. */
 
 /* lb_spmv_ex -- lb_spmv with flags (LB_SPMV_REPARTITION: the whole merge-path method --
  * partition, tile processing, fix-up -- runs in this call; used by bench.py's step). */

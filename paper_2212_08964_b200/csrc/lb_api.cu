@@ -295,6 +295,14 @@ struct lb_csr_s {
   int64_t ch_t[kChunksMax + 1] = {}, ch_i[kChunksMax + 1] = {};
   cudaStream_t ch_d2h = nullptr;
   cudaEvent_t ch_ev[kChunksMax] = {};
+  // lb_spmv_multi_ex(LB_SPMV_CHUNKED): every rank's local chunk cut rows [nranks][kChunksMax + 1]
+  // (exchanged once per communicator and tile length), the exchange stream and its done event
+  std::vector<int64_t> mc_rows;
+  const void* mc_comm = nullptr;
+  int mc_L = 0, mc_gen = -1;
+  int plan_gen = 0;             // bumped by every plan build / drop (keys the exchanged cut table)
+  cudaStream_t mc_stream = nullptr;
+  cudaEvent_t mc_done = nullptr;
   int* q_a = nullptr;          // [rows] frontier lists (ping-pong)
   int* q_b = nullptr;
   int* stamp = nullptr;        // [rows] round of the last push
@@ -728,6 +736,7 @@ lb_status_t launch_partition_xhot(const lb_csr_s* A, int64_t L, bool partition, 
 }
 
 void drop_plan(lb_csr_s* A) {
+  ++A->plan_gen;
   if (A->plan_mem) cudaFree(A->plan_mem);
   A->plan_mem = nullptr;
   A->hcol = A->hot_cols = A->warm_cols = nullptr;
@@ -1389,6 +1398,11 @@ lb_status_t lb_csr_destroy(lb_csr_t A) {
   if (A->sssp_mem) cudaFree(A->sssp_mem);
   if (A->bin_mem) cudaFree(A->bin_mem);
   if (A->hx_stage) cudaFree(A->hx_stage);
+  if (A->mc_stream) {
+    cudaStreamSynchronize(A->mc_stream);
+    cudaStreamDestroy(A->mc_stream);
+    if (A->mc_done) cudaEventDestroy(A->mc_done);
+  }
   if (A->ch_d2h) {
     cudaStreamSynchronize(A->ch_d2h);
     for (auto& e : A->ch_ev)
@@ -1606,19 +1620,11 @@ lb_status_t lb_spmv_phase_times(lb_csr_t A, lb_schedule_t sched, const float* d_
   return st;
 }
 
-// LB_SPMV_CHUNKED: the merge-path step with the hot plan as kChunks tile-kernel launches over tile
-// ranges that start and end on clean merge-path coordinates (no row split across a boundary, so each
-// launch's rows are final when it ends); the D2H copy of chunk k's rows overlaps chunk k+1.
 constexpr int kChunks = 8;
-lb_status_t host_x_chunked(lb_csr_s* A, const float* d_x, float* d_y, float* h_y, uint32_t flags, stream_t s) {
-  lb_status_t st;
-  const bool repart = !A->coords_valid || A->coords_kind != 0 || A->coords_L != A->L || (flags & LB_SPMV_REPARTITION);
-  if ((st = launch_partition_xhot(A, A->L, repart, d_x, s)) != LB_OK) return st;
-  if (repart) { A->coords_valid = true; A->coords_L = A->L; A->coords_kind = 0; }
-  if (!A->ch_d2h) {
-    LB_CUDA(cudaStreamCreateWithFlags(&A->ch_d2h, cudaStreamNonBlocking));
-    for (auto& e : A->ch_ev) LB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  }
+
+// Clean chunk cuts of A's merge-path tiles at its tile length (computed once per tile length; the
+// partition must be current).  Synchronises `s` on first use.
+lb_status_t ensure_chunks(lb_csr_s* A, stream_t s) {
   const int64_t T = num_tiles(A->rows, A->nnz, A->L);
   if (A->ch_L != A->L) {  // chunk boundaries of this tile length (deterministic: computed once)
     int* d_out = nullptr;
@@ -1639,6 +1645,22 @@ lb_status_t host_x_chunked(lb_csr_s* A, const float* d_x, float* d_y, float* h_y
     A->ch_n = n;
     A->ch_L = A->L;
   }
+  return LB_OK;
+}
+
+// LB_SPMV_CHUNKED: the merge-path step with the hot plan as kChunks tile-kernel launches over tile
+// ranges that start and end on clean merge-path coordinates (no row split across a boundary, so each
+// launch's rows are final when it ends); the D2H copy of chunk k's rows overlaps chunk k+1.
+lb_status_t host_x_chunked(lb_csr_s* A, const float* d_x, float* d_y, float* h_y, uint32_t flags, stream_t s) {
+  lb_status_t st;
+  const bool repart = !A->coords_valid || A->coords_kind != 0 || A->coords_L != A->L || (flags & LB_SPMV_REPARTITION);
+  if ((st = launch_partition_xhot(A, A->L, repart, d_x, s)) != LB_OK) return st;
+  if (repart) { A->coords_valid = true; A->coords_L = A->L; A->coords_kind = 0; }
+  if (!A->ch_d2h) {
+    LB_CUDA(cudaStreamCreateWithFlags(&A->ch_d2h, cudaStreamNonBlocking));
+    for (auto& e : A->ch_ev) LB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  if ((st = ensure_chunks(A, s)) != LB_OK) return st;
   for (int k = 0; k < A->ch_n; ++k) {
     A->tr_t0 = A->ch_t[k];
     A->tr_t1 = A->ch_t[k + 1];
@@ -1810,6 +1832,7 @@ typedef struct { char internal[128]; } nccl_uid_t;
 typedef void* nccl_comm_t;
 typedef int nccl_result_t;
 constexpr int kNcclFloat32 = 7;
+constexpr int kNcclInt32 = 2;
 
 struct NcclApi {
   bool loaded = false;
@@ -2063,6 +2086,86 @@ lb_status_t lb_spmv_multi(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, co
   return lb_spmv_multi_ex(A_local, c, sched, h_bounds, d_x_full, d_y_full, 0u, stream);
 }
 
+// lb_spmv_multi_ex(LB_SPMV_CHUNKED): the rank's hot-plan merge-path SpMV as tile-range launches cut at
+// clean coordinates (ensure_chunks); as soon as chunk c is done on every rank, an NCCL group of
+// broadcasts (root k sends its chunk c rows) runs on the handle's exchange stream while chunk c+1
+// computes (the sub-shard overlap).  Every rank learns every rank's cut rows once
+// (a group of int32 broadcasts); ranks with fewer clean cuts send empty chunks.
+lb_status_t multi_chunked(lb_csr_s* A, lb_comm_s* c, lb_schedule_t sched, const int64_t* h_bounds,
+                          const float* d_x_full, float* d_y_full, uint32_t flags, stream_t s) {
+  lb_status_t st;
+  const int64_t b0 = h_bounds[c->rank];
+  float* y_loc = d_y_full + b0;
+  // a rank that cannot run the chunked kernel (no plan, other schedule, empty shard) computes its rows
+  // in one call and sends them as chunk 0, so every rank issues the same collectives
+  const bool chunkable = sched == LB_SCHED_MERGE_PATH && hot_usable(A) && A->rows > 0;
+  if (chunkable) {
+    const bool repart = !A->coords_valid || A->coords_kind != 0 || A->coords_L != A->L || (flags & LB_SPMV_REPARTITION);
+    if ((st = launch_partition_xhot(A, A->L, repart, d_x_full, s)) != LB_OK) return st;
+    if (repart) { A->coords_valid = true; A->coords_L = A->L; A->coords_kind = 0; }
+    if ((st = ensure_chunks(A, s)) != LB_OK) return st;
+  } else if (A->rows > 0) {
+    if ((st = spmv_impl(A, sched, d_x_full, y_loc, flags, s, nullptr)) != LB_OK) return st;
+  }
+  constexpr int K1 = kChunks + 1;
+  if (!A->mc_stream) {
+    LB_CUDA(cudaStreamCreateWithFlags(&A->mc_stream, cudaStreamNonBlocking));
+    LB_CUDA(cudaEventCreateWithFlags(&A->mc_done, cudaEventDisableTiming));
+    for (auto& e : A->ch_ev)
+      if (!e) LB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  if (A->mc_comm != (const void*)c || A->mc_L != A->L || A->mc_gen != A->plan_gen ||
+      (int)A->mc_rows.size() != c->nranks * K1) {
+    int32_t mine[K1];
+    for (int k = 0; k < K1; ++k)  // padded with empty chunks
+      mine[k] = chunkable ? (int32_t)A->ch_i[std::min(k, A->ch_n)] : (k == 0 ? 0 : (int32_t)A->rows);
+    int32_t* d_all = nullptr;
+    if (cudaMalloc(&d_all, (size_t)c->nranks * K1 * 4) != cudaSuccess) { cudaGetLastError(); return fail(LB_ERR_OOM, "cuts"); }
+    struct Free { int32_t* p; ~Free() { cudaFree(p); } } free_all{d_all};
+    LB_CUDA(cudaMemcpyAsync(d_all + (size_t)c->rank * K1, mine, sizeof mine, cudaMemcpyHostToDevice, s));
+    LB_NCCL(g_nccl.GroupStart());
+    for (int k = 0; k < c->nranks; ++k) {
+      nccl_result_t r = g_nccl.Broadcast(d_all + (size_t)k * K1, d_all + (size_t)k * K1, K1, kNcclInt32, k, c->comm, s);
+      if (r != 0) { g_nccl.GroupEnd(); return fail(LB_ERR_NCCL, "ncclBroadcast: %s", g_nccl.GetErrorString(r)); }
+    }
+    LB_NCCL(g_nccl.GroupEnd());
+    std::vector<int32_t> all((size_t)c->nranks * K1);
+    LB_CUDA(cudaMemcpyAsync(all.data(), d_all, all.size() * 4, cudaMemcpyDeviceToHost, s));
+    LB_CUDA(cudaStreamSynchronize(s));
+    A->mc_rows.assign(all.begin(), all.end());
+    A->mc_comm = c;
+    A->mc_L = A->L;
+    A->mc_gen = A->plan_gen;
+  }
+  for (int ch = 0; ch < kChunks; ++ch) {
+    if (chunkable && ch < A->ch_n) {
+      A->tr_t0 = A->ch_t[ch];
+      A->tr_t1 = A->ch_t[ch + 1];
+      st = hot_launch(A, d_x_full, y_loc, s);
+      A->tr_t0 = 0;
+      A->tr_t1 = -1;
+      if (st != LB_OK) return st;
+    }
+    LB_CUDA(cudaEventRecord(A->ch_ev[ch], s));
+    LB_CUDA(cudaStreamWaitEvent(A->mc_stream, A->ch_ev[ch], 0));
+    LB_NCCL(g_nccl.GroupStart());
+    for (int k = 0; k < c->nranks; ++k) {
+      const int64_t r0 = A->mc_rows[(size_t)k * K1 + ch], r1 = A->mc_rows[(size_t)k * K1 + ch + 1];
+      if (r1 <= r0) continue;
+      float* p = d_y_full + h_bounds[k] + r0;
+      nccl_result_t r = g_nccl.Broadcast(p, p, (size_t)(r1 - r0), kNcclFloat32, k, c->comm, A->mc_stream);
+      if (r != 0) { g_nccl.GroupEnd(); return fail(LB_ERR_NCCL, "ncclBroadcast: %s", g_nccl.GetErrorString(r)); }
+    }
+    LB_NCCL(g_nccl.GroupEnd());
+  }
+  LB_CUDA(cudaEventRecord(A->mc_done, A->mc_stream));
+  LB_CUDA(cudaStreamWaitEvent(s, A->mc_done, 0));
+  nccl_result_t ar = 0;
+  LB_NCCL(g_nccl.CommGetAsyncError(c->comm, &ar));
+  if (ar != 0) return fail(LB_ERR_NCCL, "NCCL async error: %s", g_nccl.GetErrorString(ar));
+  return LB_OK;
+}
+
 lb_status_t lb_spmv_multi_ex(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, const int64_t* h_bounds,
                              const float* d_x_full, float* d_y_full, uint32_t flags, void* stream) {
   g_err.clear();
@@ -2072,6 +2175,9 @@ lb_status_t lb_spmv_multi_ex(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched,
   if (b1 - b0 != A_local->rows)
     return fail(LB_ERR_INVALID_ARG, "local shard has %lld rows, bounds say %lld", (long long)A_local->rows,
                 (long long)(b1 - b0));
+  for (int k = 0; k < c->nranks; ++k)
+    if (h_bounds[k + 1] < h_bounds[k]) return fail(LB_ERR_INVALID_ARG, "bounds not monotone at %d", k);
+  if (flags & LB_SPMV_CHUNKED) return multi_chunked(A_local, c, sched, h_bounds, d_x_full, d_y_full, flags, S(stream));
   lb_status_t st = spmv_impl(A_local, sched, d_x_full, d_y_full + b0, flags, S(stream), nullptr);
   if (st != LB_OK) return st;
   return lb_allgather_rows(c, h_bounds, d_y_full, stream);

@@ -467,11 +467,15 @@ class Comm:
             pass
 
     def spmv_multi(self, A_local: CsrMatrix, bounds, x_full: torch.Tensor, y_full: torch.Tensor,
-                   schedule="merge_path", stream=None, repartition: bool = False) -> torch.Tensor:
+                   schedule="merge_path", stream=None, repartition: bool = False,
+                   chunked: bool = False) -> torch.Tensor:
+        """lb_spmv_multi(_ex).  chunked: LB_SPMV_CHUNKED -- each chunk's rows are all-gathered while the
+        next chunk computes (collective: every rank passes the same flags)."""
         b = np.ascontiguousarray(bounds, dtype=np.int64)
-        if repartition:
+        if repartition or chunked:
+            flags = (LB_SPMV_REPARTITION if repartition else 0) | (LB_SPMV_CHUNKED if chunked else 0)
             _check(lib().lb_spmv_multi_ex(A_local.handle, self._c, _sched(schedule), b.ctypes.data, x_full.data_ptr(),
-                                          y_full.data_ptr(), LB_SPMV_REPARTITION, _stream(stream)))
+                                          y_full.data_ptr(), flags, _stream(stream)))
         else:
             _check(lib().lb_spmv_multi(A_local.handle, self._c, _sched(schedule), b.ctypes.data, x_full.data_ptr(),
                                        y_full.data_ptr(), _stream(stream)))

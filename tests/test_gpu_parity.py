@@ -412,6 +412,27 @@ def test_row_shards_concatenate_bit_identical(G):
     assert torch.equal(torch.cat(ys), full)
 
 
+@pytest.mark.parametrize("plan", [True, False])
+def test_spmv_multi_chunked_single_rank_nccl(plan):
+    """lb_spmv_multi_ex(LB_SPMV_CHUNKED) at world size 1: tile-range launches, the cut-table exchange
+    and one broadcast group per chunk on the exchange stream; bit-exact against the oracle in integer
+    mode, repeated with a new x, with and without a plan (no plan: one chunk, same collectives)."""
+    A = lbgen.rmat(14, 16, 8, "int")
+    uid = lb.Comm.unique_id()
+    comm = lb.Comm(uid, 0, 1, torch.cuda.current_device())
+    b = lb.shard_bounds(A.row_offsets, 1)
+    M = lb.CsrMatrix.from_csr(A)
+    if plan:
+        M.plan_hot_x(256, 0)
+    for it in range(3):
+        x = lbgen.make_x(A.cols, "int", 40 + it)
+        y_ref, s_ref = ref(A, x)
+        y = torch.full((A.rows,), float("nan"), device="cuda")
+        comm.spmv_multi(M, b, x.cuda(), y, "merge_path", repartition=it == 0, chunked=True)
+        torch.cuda.synchronize()
+        check_y(y, y_ref, s_ref, True, f"multi_chunked/plan{plan}/{it}")
+
+
 def test_spmv_multi_single_rank_nccl():
     A = lbgen.rmat(12, 16, 6, "int")
     x = lbgen.make_x(A.cols, "int", 6)
