@@ -1629,7 +1629,13 @@ lb_status_t ensure_chunks(lb_csr_s* A, stream_t s) {
   if (A->ch_L != A->L) {  // chunk boundaries of this tile length (deterministic: computed once)
     int* d_out = nullptr;
     if (cudaMalloc(&d_out, 2 * kChunks * sizeof(int)) != cudaSuccess) { cudaGetLastError(); return fail(LB_ERR_OOM, "chunks"); }
-    lbk::clean_tiles_kernel<<<1, 32, 0, s>>>(A->coords, A->off, T, kChunks, 4096, d_out);
+    // a hot tile-kernel launch has `wave` warps and takes ceil(tiles / wave) tiles per warp: cut after
+    // q whole waves minus a slack of 32 tiles, so a clean cut found within the slack (a clean start
+    // every ~1 + nnz/rows merge items) keeps the chunk at q waves
+    const int64_t wave = std::min(A->dev->sm_count * hot_warps(), kMaxCtas), slack = 32;
+    const int64_t q = T / ((int64_t)kChunks * wave);
+    const int64_t step = q >= 1 && q * wave > 4 * slack ? q * wave - slack : T / kChunks;
+    lbk::clean_tiles_kernel<<<1, 32, 0, s>>>(A->coords, A->off, T, kChunks, 4096, step, d_out);
     LB_LAUNCHED();
     int h[2 * kChunks] = {};
     cudaError_t e1 = cudaMemcpyAsync(h, d_out, sizeof h, cudaMemcpyDeviceToHost, s);

@@ -175,14 +175,16 @@ __global__ void partition_xhot_kernel(int rows, int nnz, const int* __restrict__
   }
 }
 
-// Chunk boundaries for lb_spmv_host_x(LB_SPMV_CHUNKED): for k = 1 .. K-1 the first tile t >= k*T/K
+// Chunk boundaries for lb_spmv_host_x(LB_SPMV_CHUNKED): for k = 1 .. K-1 the first tile t >= k*step
 // (scanning at most `span` tiles) whose start coordinate is clean -- j == off[i], no row split -- else
 // T.  out[k] = t, out[K + k] = coords[t].x (its first row).
 __global__ void clean_tiles_kernel(const int2* __restrict__ coords, const int* __restrict__ off, int64_t T, int K,
-                                   int span, int* __restrict__ out) {
+                                   int span, int64_t step, int* __restrict__ out) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x + 1;
   if (k >= K) return;
-  int64_t t = (int64_t)k * T / K, found = T;
+  // the scan starts at k*step: the host picks step a few tiles short of a whole number of waves (one
+  // tile per warp of a launch), so a chunk whose cut is found within that slack fills its waves exactly
+  int64_t t = (int64_t)k * step, found = T;
   for (int n = 0; n < span && t < T; ++n, ++t) {
     const int2 c = coords[t];
     if (c.y == __ldg(off + c.x)) { found = t; break; }
