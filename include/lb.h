@@ -15,7 +15,9 @@
  *    allocated at create time so that lb_spmv can be captured in a CUDA graph.
  *  - Asynchrony: every call is stream-ordered and does not synchronise the host, except
  *    lb_csr_create(validate=1) (one sync to read the validation flag), lb_spmv_host and
- *    lb_spmv_host_x (return with y on the host) and the lb_comm_* setup calls.
+ *    lb_spmv_host_x (return with y on the host), lb_spmv_host_x_wait, the lb_comm_* setup calls,
+ *    and the first LB_SPMV_CHUNKED call per tile length (one sync to read the chunk cuts; in
+ *    lb_spmv_multi_ex also to exchange them).
  *  - Errors: a status code is returned; no exception crosses the ABI.  lb_last_error()
  *    returns a thread-local message for the last failing call on this thread.
  *  - Index widths: int32 row offsets and column indices, fp32 values, x and y (P:963-969,
