@@ -270,6 +270,7 @@ lb_status_t lb_bins(lb_csr_t A, int32_t* d_ids, int64_t h_sizes[3], void* stream
 
 /* Flags for lb_spmv_ex. */
 #define LB_SPMV_REPARTITION 1u /* MERGE_PATH: recompute the partition inside this call */
+#define LB_SPMV_PADDED 4u      /* lb_spmv_multi_ex: padded all-gather layout (see lb_spmv_multi_ex) */
 #define LB_SPMV_CHUNKED 2u     /* lb_spmv_host_x, MERGE_PATH with an x-reuse plan: run the tile kernel as
                                   up to 8 launches over tile ranges cut at clean merge-path coordinates
                                   (no row split across a cut) and copy each range's y rows to the host
@@ -343,6 +344,18 @@ lb_status_t lb_spmv_phase_times(lb_csr_t A, lb_schedule_t sched, const float* d_
                                 float* ms_out);
 
 /*
+ * lb_csr_trace_phases -- per-call phase timing of the next `capacity` lb_spmv* calls on this handle
+ * (0 disables and frees).  Each traced call records four CUDA events on its stream (start, partition
+ * done, main kernel done, fix-up done); lb_csr_trace_read synchronises on the last one, writes
+ * ms_out[c*3 + {0,1,2}] = (partition, main, fix-up) milliseconds of traced call c (n_out calls) and
+ * resets the trace (the capacity stays).  For measuring the dominant kernel inside a timed region of
+ * back-to-back calls (bench.py); the event records may defeat the PDL overlap of partition and tile
+ * kernel, so the region's own step time is reported beside it.
+ */
+lb_status_t lb_csr_trace_phases(lb_csr_t A, int32_t capacity);
+lb_status_t lb_csr_trace_read(lb_csr_t A, int32_t* n_out, float* ms_out);
+
+/*
  * lb_probe_stream_gather -- diagnostics: time (CUDA events, synchronises `stream`) a kernel that
  * streams A's col_idx/values with the tile processor's 256-bit loads and gathers x[col] with no
  * row structure, `reps` times; ms_out = mean milliseconds per pass.  nnz / ms_out is the
@@ -397,7 +410,11 @@ lb_status_t lb_spmv_multi(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, co
                           const float* d_x_full, float* d_y_full, void* stream);
 
 /* lb_spmv_multi_ex -- lb_spmv_multi with lb_spmv_ex flags (LB_SPMV_REPARTITION: the rank's merge-path
- * partition is recomputed inside the call; bench.py's multi-GPU step). */
+ * partition is recomputed inside the call; bench.py's multi-GPU step), LB_SPMV_CHUNKED (see the flag)
+ * or LB_SPMV_PADDED (the padded all-gather layout of lb_allgather_padded: d_x_full and d_y_full are
+ * fp32[nranks * P], P = lb_padded_rows, rank r's rows at slot r * P, and A_local's column ids were
+ * remapped with lb_remap_cols_padded; exclusive with LB_SPMV_CHUNKED).  Flags must be equal on all
+ * ranks (the collectives they select must match). */
 lb_status_t lb_spmv_multi_ex(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, const int64_t* h_bounds,
                              const float* d_x_full, float* d_y_full, uint32_t flags, void* stream);
 
@@ -410,7 +427,10 @@ lb_status_t lb_spmv_multi_ex(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched,
  * lb_spmv_multi_fused then computes this rank's rows of y = A x with the merge-path tile kernel
  * writing every final y value to its own buffer AND to every peer's buffer over NVLink (rows whose
  * value the fix-up completes are sent by the fix-up), followed by a cross-rank barrier (an NCCL
- * group of 4-byte broadcasts), so that in stream order every rank's buffer holds the whole y.  If
+ * group of 4-byte broadcasts), so that in stream order every rank's buffer holds the whole y.  An
+ * entry barrier of the same kind precedes the kernel, so no rank stores into a peer's buffer before
+ * that peer's stream has finished the work queued before the call (write-after-read: e.g. copying
+ * the previous y into its x); reads of the buffer on OTHER streams must be ordered by the caller.  If
  * no fused kernel applies (schedule other than MERGE_PATH, L other than 504/1016, unaligned
  * arrays) it computes locally and exchanges with lb_allgather_rows.  x must not alias the buffer.
  * flags: LB_SPMV_REPARTITION.  lb_peer_destroy unmaps the peers (after all work completed).
@@ -429,8 +449,55 @@ lb_status_t lb_spmv_peers(lb_csr_t A, const float* d_x, float* d_y, float* const
                           uint32_t flags, void* stream);
 
 /* lb_allgather_rows -- the exchange step of lb_spmv_multi alone: rank r contributes
- * d_y_full[b_r .. b_{r+1}) and receives every other rank's slice in place. */
+ * d_y_full[b_r .. b_{r+1}) and receives every other rank's slice in place (SURVEY 8(e) option 1: one
+ * NCCL group of broadcasts with root k sending rank k's slice, scheduled by lb_exchange_schedule;
+ * at world size 1 the group holds one in-place broadcast). */
 lb_status_t lb_allgather_rows(lb_comm_t c, const int64_t* h_bounds, float* d_y_full, void* stream);
+
+/*
+ * lb_exchange_schedule -- host-only: the broadcasts of the y exchange, as every exchange path of this
+ * library issues them.  For chunk c (0 <= c < nchunks) and root rank k, rank k broadcasts
+ * y_full[h_offsets[c*nranks + k], + h_counts[c*nranks + k]) to every rank (count 0: no call).
+ *  h_bounds    int64[nranks+1] shard bounds (b_0 = 0, non-decreasing; from lb_shard_bounds).
+ *  h_cut_rows  int64[nranks][nchunks+1]: rank k's chunk c is its LOCAL rows [cut[k][c], cut[k][c+1])
+ *              (cut[k][0] = 0, cut[k][nchunks] = b_{k+1} - b_k, non-decreasing), e.g. the table
+ *              lb_spmv_multi_ex(LB_SPMV_CHUNKED) exchanges (lb_csr_chunk_rows of every rank);
+ *              NULL: one chunk holding every rank's whole slice (lb_allgather_rows).
+ * Over all (c, k) the ranges tile [0, b_G) exactly once.  LB_ERR_INVALID_ARG on bounds or cuts that
+ * are not monotone or do not span the shard.
+ */
+lb_status_t lb_exchange_schedule(int32_t nranks, const int64_t* h_bounds, int32_t nchunks, const int64_t* h_cut_rows,
+                                 int64_t* h_offsets, int64_t* h_counts);
+
+/* lb_csr_chunk_rows -- the handle's LB_SPMV_CHUNKED cut rows padded to nchunks + 1 entries (nchunks
+ * must be 8): what this rank contributes to the chunked exchange's cut table.  Computes the cuts on
+ * first use (synchronises `stream`); without a usable x-reuse plan: {0, rows, rows, ...}. */
+lb_status_t lb_csr_chunk_rows(lb_csr_t A, int32_t nchunks, int64_t* h_rows_out, void* stream);
+
+/*
+ * Padded all-gather layout (SURVEY 8(e) option 2).  P = lb_padded_rows(nranks, h_bounds) = the largest
+ * shard; y lives in fp32[nranks * P] with rank k's rows at [k*P, k*P + b_{k+1} - b_k).
+ *  lb_remap_cols_padded  global column c (in shard k: b_k <= c < b_{k+1}) -> k*P + (c - b_k), for a
+ *                        shard's col_idx (device, nnz entries; in and out may alias).  Synchronises.
+ *  lb_allgather_padded   one in-place ncclAllGather of the P-sized slots (every rank's slot r*P).
+ */
+int64_t lb_padded_rows(int32_t nranks, const int64_t* h_bounds);
+lb_status_t lb_remap_cols_padded(int32_t nranks, const int64_t* h_bounds, const int32_t* d_col_in, int64_t nnz,
+                                 int32_t* d_col_out, void* stream);
+lb_status_t lb_allgather_padded(lb_comm_t c, int64_t padded_rows, float* d_y_pad, void* stream);
+
+/*
+ * Replica check (after the exchange every rank's y must match bitwise).
+ *  lb_y_checksum           h = sum_i mix64(i * 0x9E3779B97F4A7C15 + bits(y_i)) mod 2^64, mix64 = the
+ *                          splitmix64 finaliser, bits = the fp32 bit pattern (so -0 != +0).  Order-free
+ *                          and deterministic.  Synchronises `stream`.
+ *  lb_comm_check_replicas  the same hash on every rank, NCCL all-reduces of its min and max:
+ *                          *h_equal = 1 iff every rank's d_y[0, n) hashes equal.  Collective;
+ *                          synchronises `stream`.
+ */
+lb_status_t lb_y_checksum(const float* d_y, int64_t n, void* stream, uint64_t* h_out);
+lb_status_t lb_comm_check_replicas(lb_comm_t c, const float* d_y, int64_t n, void* stream, int32_t* h_equal,
+                                   uint64_t* h_hash);
 
 /* Name of the main kernel lb_spmv(A, sched) launches with the handle's current settings
  * (diagnostics / bench reporting); "" for an unknown schedule. */

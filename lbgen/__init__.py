@@ -71,6 +71,8 @@ def values_from_bits(u: torch.Tensor, mode: str) -> torch.Tensor:
         return (sign * mag).to(torch.float32)
     if mode == "xint":
         return ((u % 9) - 4).to(torch.float32)
+    if mode == "pos":  # same-sign: uniform [0, 1) on the 2^-24 grid (exact in fp32)
+        return (u.to(torch.float64) * 2.0 ** -24).to(torch.float32)
     raise ValueError(mode)
 
 
@@ -119,6 +121,8 @@ def _offsets_from_lengths(lengths: torch.Tensor) -> torch.Tensor:
 def assign_values(nnz: int, mode: str, seed: int, device) -> torch.Tensor:
     if mode == "ones":
         return torch.ones(nnz, dtype=torch.float32, device=device)
+    if mode == "tenth":  # same-sign constant fl32(0.1): the worst case for sequential fp32 sums
+        return torch.full((nnz,), 0.1, dtype=torch.float32, device=device)
     out = torch.empty(nnz, dtype=torch.float32, device=device)
     chunk = 1 << 26
     for s in range(0, nnz, chunk):

@@ -29,6 +29,30 @@ def build(force: bool = False) -> str:
 
 
 _lib = None
+_timing = None
+
+
+def timing_lib():
+    """The same oracle.c built for TIMING on this host (bench.py's cpu_baseline / reference arm only):
+    -O3 -march=native -fopenmp, still -ffp-contract=off and no fast-math (the summation order and
+    rounding are the definition's).  Built fresh per process into a temporary directory, so a library
+    compiled for another host's ISA is never loaded."""
+    global _timing
+    if _timing is None:
+        import tempfile
+        d = tempfile.mkdtemp(prefix="oracle_native_")
+        out = os.path.join(d, "liboracle_native.so")
+        subprocess.check_call(["gcc", "-O3", "-march=native", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+                               "-fPIC", "-shared", "-o", out, _SRC])
+        L = ctypes.CDLL(out)
+        i64, p = ctypes.c_int64, ctypes.c_void_p
+        L.oracle_spmv.argtypes = [i64, p, p, p, p, p, p]
+        L.oracle_spmv_omp.argtypes = [i64, p, p, p, p, p, p]
+        L.oracle_partition.argtypes = [i64, i64, p, i64, p]
+        L.oracle_partition.restype = i64
+        L.oracle_num_threads.restype = ctypes.c_int
+        _timing = L
+    return _timing
 
 
 def lib():
@@ -68,8 +92,9 @@ def _ptr(a: np.ndarray):
     return a.ctypes.data_as(ctypes.c_void_p)
 
 
-def spmv(row_offsets, col_idx, values, x, threads: bool = False):
-    """y = A x in double, plus s_i = sum_k |a_ik x_k|.  Returns (y, s) as float64 arrays."""
+def spmv(row_offsets, col_idx, values, x, threads: bool = False, timing: bool = False):
+    """y = A x in double, plus s_i = sum_k |a_ik x_k|.  Returns (y, s) as float64 arrays.
+    timing: run the -O3 -march=native build (timing_lib; same arithmetic)."""
     off = _np(row_offsets, np.int32)
     col = _np(col_idx, np.int32)
     val = _np(values, np.float32)
@@ -77,7 +102,8 @@ def spmv(row_offsets, col_idx, values, x, threads: bool = False):
     rows = off.size - 1
     y = np.empty(rows, np.float64)
     s = np.empty(rows, np.float64)
-    f = lib().oracle_spmv_omp if threads else lib().oracle_spmv
+    L = timing_lib() if timing else lib()
+    f = L.oracle_spmv_omp if threads else L.oracle_spmv
     f(rows, _ptr(off), _ptr(col), _ptr(val), _ptr(xx), _ptr(y), _ptr(s))
     return y, s
 
@@ -109,14 +135,14 @@ def spmv_packed(sel_offsets, sel_cols, sel_vals, x):
     return y, s
 
 
-def partition(row_offsets, L: int) -> np.ndarray:
+def partition(row_offsets, L: int, timing: bool = False) -> np.ndarray:
     """Brute-force merge-path tile coordinates: int32 array [T+1, 2] of (row, nz)."""
     off = _np(row_offsets, np.int32)
     rows = off.size - 1
     nnz = int(off[-1]) if rows > 0 else 0
     T = (rows + nnz + L - 1) // L
     out = np.empty((T + 1, 2), np.int32)
-    got = lib().oracle_partition(rows, nnz, _ptr(off), L, _ptr(out))
+    got = (timing_lib() if timing else lib()).oracle_partition(rows, nnz, _ptr(off), L, _ptr(out))
     if got != T:
         raise ValueError("bad partition arguments")
     return out

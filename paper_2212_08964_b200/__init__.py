@@ -2,5 +2,7 @@
 
 The compute path is liblb.so (include/lb.h, csrc/); this package is its thin binding.
 """
-from .lb import (LIB_PATH, CsrMatrix, Comm, HostSpmv, InvalidCsr, LbError, SCHEDULES, declared_functions,  # noqa: F401
-                 gather_slices, last_error, launch_count, lib, shard_bounds, shard_csr, spmv, version)
+from .lb import (CHUNKS_MAX, LIB_PATH, SCHEDULES, TILE_LENGTHS, Comm, CsrMatrix, HostSpmv,  # noqa: F401
+                 InvalidCsr, LbError, PeerBuffer, declared_functions, exchange_schedule, gather_slices, last_error,
+                 launch_count, lib, padded_rows, remap_cols_padded, shard_bounds, shard_csr, spmv, version,
+                 y_checksum)

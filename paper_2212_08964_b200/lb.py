@@ -24,6 +24,8 @@ SCHEDULES = {"thread_mapped": 0, "group_mapped": 1, "merge_path": 2, "block_mapp
 SCHEDULE_NAMES = {v: k for k, v in SCHEDULES.items()}
 LB_SPMV_REPARTITION = 1
 LB_SPMV_CHUNKED = 2
+LB_SPMV_PADDED = 4
+CHUNKS_MAX = 8
 DEFAULT_ITEMS_PER_TILE = 1016
 TILE_LENGTHS = (504, 1016, 2040, 3064, 4088)
 
@@ -79,6 +81,8 @@ def lib() -> ctypes.CDLL:
         "lb_spmv_phase_times": ([p, ctypes.c_int, p, p, p, ctypes.POINTER(ctypes.c_float)], st),
         "lb_probe_stream_gather": ([p, p, i32, p, ctypes.POINTER(ctypes.c_float)], st),
         "lb_probe_stream": ([p, i32, p, ctypes.POINTER(ctypes.c_float)], st),
+        "lb_csr_trace_phases": ([p, i32], st),
+        "lb_csr_trace_read": ([p, ctypes.POINTER(i32), ctypes.POINTER(ctypes.c_float)], st),
         "lb_spmv_host_x": ([p, i32, p, p, ctypes.c_uint32, p], st),
         "lb_spmv_host_x_async": ([p, i32, p, p, ctypes.c_uint32, p], st),
         "lb_spmv_host_x_wait": ([p], st),
@@ -89,6 +93,13 @@ def lib() -> ctypes.CDLL:
         "lb_spmv_multi": ([p, p, ctypes.c_int, p, p, p, p], st),
         "lb_spmv_multi_ex": ([p, p, ctypes.c_int, p, p, p, u32, p], st),
         "lb_allgather_rows": ([p, p, p, p], st),
+        "lb_exchange_schedule": ([i32, p, i32, p, p, p], st),
+        "lb_csr_chunk_rows": ([p, i32, p, p], st),
+        "lb_padded_rows": ([i32, p], i64),
+        "lb_remap_cols_padded": ([i32, p, p, i64, p, p], st),
+        "lb_allgather_padded": ([p, i64, p, p], st),
+        "lb_y_checksum": ([p, i64, p, ctypes.POINTER(ctypes.c_uint64)], st),
+        "lb_comm_check_replicas": ([p, p, i64, p, ctypes.POINTER(i32), ctypes.POINTER(ctypes.c_uint64)], st),
         "lb_peer_create": ([p, p, i64, p, ctypes.POINTER(p)], st),
         "lb_peer_destroy": ([p], st),
         "lb_spmv_multi_fused": ([p, p, ctypes.c_int, p, p, u32, p], st),
@@ -173,6 +184,7 @@ class CsrMatrix:
                                        _stream(stream), ctypes.byref(self._h)))
         self.device = self.row_offsets.device
         self.items_per_tile = 2040 if self.nnz < 8 * self.rows else DEFAULT_ITEMS_PER_TILE
+        self._host_refs = []  # host tensors of enqueued spmv_host_async calls (alive until spmv_host_wait)
 
     @classmethod
     def from_csr(cls, A, device="cuda", validate: bool = True) -> "CsrMatrix":
@@ -188,8 +200,9 @@ class CsrMatrix:
 
     def close(self):
         if getattr(self, "_h", None):
-            lib().lb_csr_destroy(self._h)
+            lib().lb_csr_destroy(self._h)  # synchronises the handle's copy streams first
             self._h = ctypes.c_void_p()
+        self._host_refs = []
 
     def __del__(self):
         try:
@@ -279,11 +292,21 @@ class CsrMatrix:
         _check(lib().lb_spmv_host_x_async(self.handle, _sched(schedule), h_x.data_ptr() if h_x.numel() else None,
                                           h_y.data_ptr() if h_y.numel() else None, 1 if repartition else 0,
                                           _stream(stream)))
+        # the copies run on the library's own streams, which PyTorch's caching host allocator does not
+        # track: keep both tensors alive until spmv_host_wait
+        self._host_refs.append((h_x, h_y))
         return h_y
 
     def spmv_host_wait(self) -> None:
         """lb_spmv_host_x_wait: block until every enqueued spmv_host_async's y is on the host."""
         _check(lib().lb_spmv_host_x_wait(self.handle))
+        self._host_refs = []
+
+    def chunk_rows(self, stream=None) -> np.ndarray:
+        """The handle's LB_SPMV_CHUNKED cut rows padded to CHUNKS_MAX + 1 entries (lb_csr_chunk_rows)."""
+        out = np.zeros(CHUNKS_MAX + 1, np.int64)
+        _check(lib().lb_csr_chunk_rows(self.handle, CHUNKS_MAX, out.ctypes.data, _stream(stream)))
+        return out
 
     def probe_stream(self, reps: int = 20, stream=None) -> float:
         """Milliseconds of one read-only pass over col_idx + values (lb_probe_stream)."""
@@ -360,6 +383,19 @@ class CsrMatrix:
                                      _stream(stream)))
         return hot, warm, hcol
 
+    def trace_phases(self, capacity: int) -> None:
+        """lb_csr_trace_phases: record per-phase CUDA events for the next `capacity` SpMV calls."""
+        _check(lib().lb_csr_trace_phases(self.handle, int(capacity)))
+        self._trace_cap = int(capacity)
+
+    def trace_read(self) -> np.ndarray:
+        """lb_csr_trace_read: [n, 3] (partition, main, fix-up) ms of the traced calls; resets the trace."""
+        cap = getattr(self, "_trace_cap", 0)
+        buf = (ctypes.c_float * max(3 * cap, 3))()
+        n = ctypes.c_int32()
+        _check(lib().lb_csr_trace_read(self.handle, ctypes.byref(n), buf))
+        return np.frombuffer(buf, dtype=np.float32, count=3 * n.value).reshape(n.value, 3).astype(np.float64)
+
     def kernel_name(self, schedule="merge_path") -> str:
         """Main kernel lb_spmv launches for `schedule` (lb_kernel_name)."""
         return lib().lb_kernel_name(self.handle, _sched(schedule)).decode()
@@ -410,9 +446,54 @@ def shard_bounds(row_offsets, nranks: int) -> np.ndarray:
     return out
 
 
+def exchange_schedule(bounds, cut_rows=None) -> tuple[np.ndarray, np.ndarray]:
+    """The broadcasts of the y exchange (lb_exchange_schedule, host-only): (offsets, counts), each int64
+    [nchunks, nranks]; chunk c, root k broadcasts y_full[offsets[c, k] : offsets[c, k] + counts[c, k]].
+    cut_rows: int64 [nranks, nchunks + 1] local cut rows of every rank (None: one chunk, the plain
+    all-gather of lb_allgather_rows)."""
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    G = b.size - 1
+    cuts = None if cut_rows is None else np.ascontiguousarray(cut_rows, dtype=np.int64)
+    K = 1 if cuts is None else cuts.shape[1] - 1
+    if cuts is not None and cuts.shape[0] != G:
+        raise ValueError("cut_rows must be [nranks, nchunks + 1]")
+    off = np.empty((K, G), np.int64)
+    cnt = np.empty((K, G), np.int64)
+    _check(lib().lb_exchange_schedule(G, b.ctypes.data, K, None if cuts is None else cuts.ctypes.data,
+                                      off.ctypes.data, cnt.ctypes.data))
+    return off, cnt
+
+
 def gather_slices(bounds) -> list[tuple[int, int]]:
     """The y slice [b_k, b_{k+1}) each rank k contributes to the all-gather (lb_allgather_rows)."""
-    return [(int(bounds[k]), int(bounds[k + 1])) for k in range(len(bounds) - 1)]
+    off, cnt = exchange_schedule(bounds)
+    return [(int(o), int(o + c)) for o, c in zip(off[0], cnt[0])]
+
+
+def padded_rows(bounds) -> int:
+    """P = the largest shard: the slot size of the padded all-gather layout (lb_padded_rows)."""
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    return int(lib().lb_padded_rows(b.size - 1, b.ctypes.data))
+
+
+def remap_cols_padded(bounds, col_idx: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """A shard's global column ids -> padded-layout ids k*P + (c - b_k) (lb_remap_cols_padded)."""
+    _dev_tensor(col_idx, torch.int32, "col_idx")
+    if out is None:
+        out = torch.empty_like(col_idx)
+    _dev_tensor(out, torch.int32, "out", col_idx.numel())
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    _check(lib().lb_remap_cols_padded(b.size - 1, b.ctypes.data, col_idx.data_ptr() if col_idx.numel() else None,
+                                      col_idx.numel(), out.data_ptr() if out.numel() else None, _stream(stream)))
+    return out
+
+
+def y_checksum(y: torch.Tensor, stream=None) -> int:
+    """lb_y_checksum: sum_i mix64(i * 0x9E3779B97F4A7C15 + bits(y_i)) mod 2^64 (include/lb.h)."""
+    _dev_tensor(y, torch.float32, "y")
+    h = ctypes.c_uint64()
+    _check(lib().lb_y_checksum(y.data_ptr() if y.numel() else None, y.numel(), _stream(stream), ctypes.byref(h)))
+    return int(h.value)
 
 
 def shard_csr(row_offsets: torch.Tensor, col_idx: torch.Tensor, values: torch.Tensor, bounds, rank: int):
@@ -468,12 +549,22 @@ class Comm:
 
     def spmv_multi(self, A_local: CsrMatrix, bounds, x_full: torch.Tensor, y_full: torch.Tensor,
                    schedule="merge_path", stream=None, repartition: bool = False,
-                   chunked: bool = False) -> torch.Tensor:
+                   chunked: bool = False, padded: bool = False) -> torch.Tensor:
         """lb_spmv_multi(_ex).  chunked: LB_SPMV_CHUNKED -- each chunk's rows are all-gathered while the
-        next chunk computes (collective: every rank passes the same flags)."""
+        next chunk computes; padded: LB_SPMV_PADDED -- x_full / y_full are nranks * padded_rows(bounds)
+        long and A_local's columns were remapped with remap_cols_padded (collective: every rank passes the
+        same flags)."""
         b = np.ascontiguousarray(bounds, dtype=np.int64)
-        if repartition or chunked:
-            flags = (LB_SPMV_REPARTITION if repartition else 0) | (LB_SPMV_CHUNKED if chunked else 0)
+        n_full = int(b[-1])
+        if padded:
+            n_full = self.nranks * padded_rows(b)
+        _dev_tensor(x_full, torch.float32, "x_full", n_full if padded else A_local.cols)
+        _dev_tensor(y_full, torch.float32, "y_full", n_full)
+        if int(b[self.rank + 1] - b[self.rank]) != A_local.rows:
+            raise ValueError("A_local's rows do not match bounds[rank + 1] - bounds[rank]")
+        if repartition or chunked or padded:
+            flags = ((LB_SPMV_REPARTITION if repartition else 0) | (LB_SPMV_CHUNKED if chunked else 0) |
+                     (LB_SPMV_PADDED if padded else 0))
             _check(lib().lb_spmv_multi_ex(A_local.handle, self._c, _sched(schedule), b.ctypes.data, x_full.data_ptr(),
                                           y_full.data_ptr(), flags, _stream(stream)))
         else:
@@ -488,14 +579,31 @@ class Comm:
                          schedule="merge_path", repartition: bool = False, stream=None) -> torch.Tensor:
         """lb_spmv_multi_fused: shard SpMV whose epilogue writes y into every rank's registered buffer."""
         b = np.ascontiguousarray(bounds, dtype=np.int64)
+        _dev_tensor(x_full, torch.float32, "x_full", A_local.cols)
         _check(lib().lb_spmv_multi_fused(A_local.handle, peer._p, _sched(schedule), b.ctypes.data, x_full.data_ptr(),
                                          LB_SPMV_REPARTITION if repartition else 0, _stream(stream)))
         return peer.y
 
     def allgather_rows(self, bounds, y_full: torch.Tensor, stream=None) -> torch.Tensor:
         b = np.ascontiguousarray(bounds, dtype=np.int64)
+        _dev_tensor(y_full, torch.float32, "y_full", int(b[-1]))
         _check(lib().lb_allgather_rows(self._c, b.ctypes.data, y_full.data_ptr(), _stream(stream)))
         return y_full
+
+    def allgather_padded(self, bounds, y_pad: torch.Tensor, stream=None) -> torch.Tensor:
+        """lb_allgather_padded: one ncclAllGather of the padded slots (slot r = y_pad[r*P : (r+1)*P])."""
+        P = padded_rows(bounds)
+        _dev_tensor(y_pad, torch.float32, "y_pad", self.nranks * P)
+        _check(lib().lb_allgather_padded(self._c, P, y_pad.data_ptr(), _stream(stream)))
+        return y_pad
+
+    def check_replicas(self, y: torch.Tensor, stream=None) -> tuple[bool, int]:
+        """lb_comm_check_replicas: (every rank's y is bitwise equal, this rank's hash)."""
+        _dev_tensor(y, torch.float32, "y")
+        eq, h = ctypes.c_int32(), ctypes.c_uint64()
+        _check(lib().lb_comm_check_replicas(self._c, y.data_ptr() if y.numel() else None, y.numel(), _stream(stream),
+                                            ctypes.byref(eq), ctypes.byref(h)))
+        return bool(eq.value), int(h.value)
 
 
 class PeerBuffer:

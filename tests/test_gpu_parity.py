@@ -7,8 +7,7 @@ Bars (BASELINE.json north_star):
   * y in tolerance mode (values and x uniform in [-1,1) on a 2^-23 grid):
     |y_gpu - y_ref| <= 1e-5 * s_ref + 1e-30 per row, s_ref = sum_k |a_ik x_k|.
 Sizes span several tiles and ragged tails; full BASELINE.json sizes are covered by
-test_full_size_configs (partition bit-exact on every tile, y on every row for C1-C4 and on
-sampled rows for C5).
+test_full_size_configs (partition bit-exact on every tile, every schedule on every row of C1-C5).
 """
 import ctypes
 
@@ -475,61 +474,67 @@ def _packed(A_dev: lbgen.Csr, sel: np.ndarray):
 @pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c4", "c5"])
 def test_full_size_configs(cfg):
     """Every schedule at the BASELINE.json size of each config (merge-path at the launch
-    configuration bench.py times): partition bit-exact on every tile; integer mode bit-exact on
-    every row (C1-C4) or on sampled rows (C5); tolerance mode on sampled rows."""
+    configuration bench.py times), against the oracle on EVERY row: partition bit-exact on every
+    tile; integer mode bit-exact; tolerance mode within 1e-5 * s + 1e-30."""
     torch.cuda.empty_cache()
-    scheds = SCHEDS if cfg != "c5" else ["merge_path", "group_mapped"]
     for vmode in ("int", "float"):
         A = lbgen.make_config(cfg, vmode, device="cuda")
         x = lbgen.x_for_config(cfg, A.cols, vmode, device="cuda")
         M = lb.CsrMatrix.from_csr(A, device="cuda")
+        coords = M.partition().cpu().numpy()
         if vmode == "int":
-            coords = M.partition().cpu().numpy()
             assert np.array_equal(coords, oracle.partition(A.row_offsets.cpu(), M.items_per_tile)), "partition"
-        else:
-            coords = M.partition().cpu().numpy()
-        full = vmode == "int" and cfg != "c5"
-        if full:
-            y_ref, s_ref = oracle.spmv(A.row_offsets.cpu(), A.col_idx.cpu(), A.values.cpu(), x.cpu(), threads=True)
-            sel = None
-        else:
-            sel = _sample_rows(A, coords, 20_000, 1)
-            so, sc, sv = _packed(A, sel)
-            y_ref, s_ref = oracle.spmv_packed(so, sc, sv, x.cpu())
-        for sched in scheds:
+        del coords
+        y_ref, s_ref = oracle.spmv(A.row_offsets.cpu(), A.col_idx.cpu(), A.values.cpu(), x.cpu(), threads=True)
+        for sched in SCHEDS:
             y = torch.full((A.rows,), float("nan"), device="cuda")
             M.spmv(x, y, sched, repartition=True)
             torch.cuda.synchronize()
-            yy = y if sel is None else y[torch.as_tensor(sel, device="cuda")]
-            check_y(yy, y_ref, s_ref, vmode == "int", f"{cfg}/{vmode}/{sched}")
-        del M, A, x
+            check_y(y, y_ref, s_ref, vmode == "int", f"{cfg}/{vmode}/{sched}")
+            del y
+        del M, A, x, y_ref, s_ref
         torch.cuda.empty_cache()
 
 
-# ---------------------------------------------------------------- every tile-kernel variant
-VARIANTS = [(0, 1016), (1, 2040), (2, 4088), (3, 504), (4, 3064), (5, 1016), (6, 1016), (7, 504), (8, 504),
-            (9, 1016), (10, 1016), (11, 2040), (12, 504), (13, 1016)]
+# ---------------------------------------------------------------- every tile kernel
 
-
-@pytest.mark.parametrize("variant,L", VARIANTS)
-def test_every_merge_variant(variant, L, monkeypatch):
-    """Each merge-path tile-kernel configuration (LB_PIPE_VARIANT) is bit-exact in integer mode
-    and within tolerance in float mode, on R-MAT, skewed and edge-case matrices."""
-    monkeypatch.setenv("LB_PIPE_VARIANT", str(variant))
+@pytest.mark.parametrize("aligned", [True, False])
+@pytest.mark.parametrize("L", [504, 1016, 2040, 3064, 4088])
+def test_every_tile_kernel(L, aligned):
+    """The tile processor of each tile length (32-byte aligned col/val: warp-streamed or CTA tiles;
+    otherwise the 128-bit / scalar fallback + fix-up kernel) is bit-exact in integer mode and within
+    tolerance in float mode, on R-MAT, skewed and edge-case matrices."""
     cases = [("rmat", lambda vm: lbgen.rmat(13, 16, 5, vm)),
              ("skewed", lambda vm: lbgen.skewed(1 << 12, 3, 30_000, 20_000, 8, vm)),
              ("stencil", lambda vm: lbgen.stencil(70, 2, vm))]
+
+    def run_L(A, x):
+        if aligned:
+            M = lb.CsrMatrix.from_csr(A)
+        else:  # col / val one element past a 32-byte boundary
+            col = torch.zeros(A.nnz + 1, dtype=torch.int32, device="cuda")
+            val = torch.zeros(A.nnz + 1, device="cuda")
+            col[1:] = A.col_idx.cuda()
+            val[1:] = A.values.cuda()
+            M = lb.CsrMatrix(A.rows, A.cols, A.row_offsets.cuda(), col[1:], val[1:])
+        M.set_items_per_tile(L)
+        assert M.kernel_name().startswith("merge_tile_kernel") != aligned or A.nnz == 0, M.kernel_name()
+        y = torch.full((A.rows,), float("nan"), device="cuda")
+        M.spmv(x.cuda(), y, "merge_path", repartition=True)
+        torch.cuda.synchronize()
+        return y
+
     for name, mk in cases:
         for vm in ("int", "float"):
             A = mk(vm)
             x = lbgen.make_x(A.cols, vm, 9)
             y_ref, s_ref = ref(A, x)
-            check_y(run(A, x, "merge_path", L), y_ref, s_ref, vm == "int", f"v{variant}/{name}/{vm}")
+            check_y(run_L(A, x), y_ref, s_ref, vm == "int", f"L{L}/{aligned}/{name}/{vm}")
     for name, A in {"giant": _csr([0, 100_003], 1), "no_nnz": _csr([0] * 3001, 3),
                     "golden": _csr([0, 1, 3, 3, 6], 1)}.items():
         x = torch.ones(A.cols)
         y_ref, s_ref = ref(A, x)
-        check_y(run(A, x, "merge_path", L), y_ref, s_ref, True, f"v{variant}/{name}")
+        check_y(run_L(A, x), y_ref, s_ref, True, f"L{L}/{aligned}/{name}")
 
 
 # ---------------------------------------------------------------- binning (Alg.4, NEXT-3)
