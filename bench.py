@@ -50,6 +50,8 @@ def parse():
                     help="multi-GPU step with LB_SPMV_CHUNKED: each chunk's rows all-gathered while the next computes")
     ap.add_argument("--fused", action="store_true",
                     help="multi-GPU step with the all-gather fused into the tile kernel (lb_spmv_multi_fused)")
+    ap.add_argument("--classes", default="c2,c4,c5",
+                    help="extra matrix classes reported beside the headline at N=1 ('' = none)")
     ap.add_argument("--hot-slots", type=int, default=0,
                     help="hot-column plan (lb_csr_plan_hot_x) slot budget: 0 = library default, -1 = no plan")
     return ap.parse_args()
@@ -145,6 +147,100 @@ def dist_env():
     return world, rank, local
 
 
+# ----------------------------------------------------------------------------- per-class reporting
+
+def graph_median(fn, reps: int = 50, warm: int = 5):
+    """median over `reps` back-to-back replays of one CUDA-graph-captured call, each
+    bracketed by CUDA events on the capturing stream, after `warm` warm-up replays."""
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            fn()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        fn()
+    for _ in range(warm):
+        g.replay()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    torch.cuda.synchronize()
+    for a, b in evs:
+        a.record()
+        g.replay()
+        b.record()
+    torch.cuda.synchronize()
+    ts = sorted(a.elapsed_time(b) for a, b in evs)
+    del g
+    return float(np.median(ts)), float(ts[0]), float(ts[-1])
+
+
+def traced_kernel_ms(M, x, y, sched, n: int = 50) -> float:
+    """Mean duration of the main kernel over n back-to-back steps (lb_csr_trace_phases: CUDA events on
+    the launch stream around each call's tile kernel)."""
+    M.trace_phases(n)
+    for _ in range(n):
+        M.spmv(x, y, sched, repartition=True)
+    tr = M.trace_read()
+    M.trace_phases(0)
+    return float(np.mean(tr[:, 1]))
+
+
+def class_report(cfg: str, dev, reps: int = 50) -> dict:
+    """BASELINE's metric is per matrix class: the step rate of merge-path (plain CSR and with the x-reuse
+    plan), of the schedule AUTO picks, the dominant kernel's roofline fraction and its ncu DRAM bytes."""
+    import paper_2212_08964_b200 as lb
+    A = lbgen.make_config(cfg, "float", device=dev)
+    x = lbgen.x_for_config(cfg, A.cols, "float", device=dev)
+    rows, cols, nnz = A.rows, A.cols, A.nnz
+    M = lb.CsrMatrix.from_csr(A, device=dev, validate=True)
+    del A
+    y = torch.empty(rows, device=dev)
+    alg = compulsory_bytes(rows, cols, nnz)
+    peak, _ = peak_hbm()
+    out = {"desc": lbgen.CONFIG_DESC.get(cfg, cfg), "rows": rows, "nnz": nnz, "algorithmic_bytes": alg,
+           "timing": f"median of {reps} CUDA-graph replays of one lb_spmv_ex(REPARTITION) step (CUDA events)"}
+
+    def entry(sched):
+        med, lo, hi = graph_median(lambda: M.spmv(x, y, sched, repartition=True), reps)
+        kms = traced_kernel_ms(M, x, y, sched)
+        return {"value": round(nnz / (med * 1e-3) / 1e9, 2), "unit": "GNZ/s", "ms": round(med, 5),
+                "ms_min_max": [round(lo, 5), round(hi, 5)], "kernel": M.kernel_name(sched),
+                "kernel_ms": round(kms, 5), "roofline_frac": round(alg / (kms * 1e-3) / 1e9 / peak, 4)}
+
+    auto = M.select_schedule()
+    out["auto_schedule"] = auto
+    out["merge_path_no_plan"] = entry("merge_path")
+    out["merge_path_no_plan"]["traffic"] = ncu_traffic(cfg, "merge_path", M.items_per_tile,
+                                                       out["merge_path_no_plan"]["kernel"])
+    if auto != "merge_path":
+        out["auto"] = entry(auto)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    hot_n, hot_nnz = M.plan_hot_x(0)
+    torch.cuda.synchronize()
+    build_ms = (time.perf_counter() - t0) * 1e3
+    if hot_n:
+        info = M.plan_info()
+        e = entry("merge_path")
+        e["traffic"] = ncu_traffic(cfg, "merge_path", M.items_per_tile, e["kernel"], hot_n)
+        e["plan"] = {"hot_cols": hot_n, "hot_nnz_frac": round(hot_nnz / max(nnz, 1), 4),
+                     "warm_cols": info["warm_cols"], "warm_nnz_frac": round(info["warm_nnz"] / max(nnz, 1), 4),
+                     "build_ms": round(build_ms, 2)}
+        gain = out["merge_path_no_plan"]["ms"] - e["ms"]
+        e["plan"]["break_even_steps"] = int(np.ceil(build_ms / gain)) if gain > 0 else None
+        out["merge_path_plan"] = e
+    else:
+        out["merge_path_plan"] = {"skipped": "lb_csr_plan_hot_x found no column worth a slot"}
+    M.plan_hot_x(-1)
+    best = max((v for k, v in out.items() if isinstance(v, dict) and "value" in v), key=lambda v: v["value"])
+    out["best"] = {"value": best["value"], "kernel": best["kernel"]}
+    del M, x, y
+    torch.cuda.empty_cache()
+    return out
+
+
 # ----------------------------------------------------------------------------- reference arm (CPU oracle)
 
 def cpu_sample(A: lbgen.Csr, x: torch.Tensor, target_nnz: int):
@@ -157,16 +253,19 @@ def cpu_sample(A: lbgen.Csr, x: torch.Tensor, target_nnz: int):
     return o, A.col_idx[:n].cpu(), A.values[:n].cpu(), x.cpu(), r, n
 
 
-def time_oracle(sample, seconds: float, min_reps: int = 1):
+def time_oracle(sample, seconds: float, min_reps: int = 5):
+    """The oracle SpMV (OpenMP over rows, fp64, the -O3 -march=native build of the same oracle.c) on the
+    sample: median over >= min_reps repetitions, repeating until `seconds` have passed."""
     import oracle
     o, c, v, xx, r, n = sample
-    oracle.spmv(o, c, v, xx, threads=True)  # warm
-    reps, t0 = 0, time.perf_counter()
-    while reps < min_reps or time.perf_counter() - t0 < seconds:
-        oracle.spmv(o, c, v, xx, threads=True)
-        reps += 1
-    dt = time.perf_counter() - t0
-    return n * reps / dt / 1e9, reps, dt
+    oracle.spmv(o, c, v, xx, threads=True, timing=True)  # warm (and builds the native copy)
+    ts, t_all = [], time.perf_counter()
+    while len(ts) < min_reps or time.perf_counter() - t_all < seconds:
+        t0 = time.perf_counter()
+        oracle.spmv(o, c, v, xx, threads=True, timing=True)
+        ts.append(time.perf_counter() - t0)
+    med = float(np.median(ts))
+    return n / med / 1e9, len(ts), time.perf_counter() - t_all
 
 
 def cpu_model() -> str:
@@ -195,7 +294,7 @@ def oracle_extras(sample, seconds: float) -> dict:
             ts.append(time.perf_counter() - t0)
         return float(np.median(ts)), len(ts)
 
-    t1, n1 = med(lambda: oracle.spmv(o, c, v, xx, threads=False))
+    t1, n1 = med(lambda: oracle.spmv(o, c, v, xx, threads=False, timing=True))
     tp, npart = med(lambda: oracle.partition(o, 1016))
     return {"cpu_model": cpu_model(), "os_cpu_count": os.cpu_count(),
             "single_thread": {"value": round(n / t1 / 1e9, 4), "unit": "GNZ/s", "reps": n1,
@@ -215,13 +314,13 @@ def run_reference(args, cfg):
     sample = cpu_sample(A, x, 16_000_000 if cfg != "c1" else A.nnz)
     o, c, v, xx, r, n = sample
     for _ in range(args.warmup):
-        oracle.spmv(o, c, v, xx, threads=True)
+        oracle.spmv(o, c, v, xx, threads=True, timing=True)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.spmv(o, c, v, xx, threads=True)
+        oracle.spmv(o, c, v, xx, threads=True, timing=True)
     dt = time.perf_counter() - t0
     val = n * args.steps / dt / 1e9
-    desc = f"leading {r} rows ({n} nnz) of {cfg}, full x; oracle.spmv_omp (fp64) per step"
+    desc = f"leading {r} rows ({n} nnz) of {cfg}, full x; oracle.spmv_omp (fp64, gcc -O3 -march=native) per step"
     print(json.dumps({
         "impl": "reference", "metric": "SpMV GNZ/s", "value": round(val, 4), "unit": "GNZ/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
@@ -292,6 +391,9 @@ def run_single(args, cfg):
         torch.cuda.synchronize()
     n0 = lb.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # every timed step records CUDA events on the launch stream around its kernels
+    # (lb_csr_trace_phases), so the dominant kernel's duration is measured inside the timed region
+    M.trace_phases(args.steps)
     torch.cuda.synchronize()
     e0.record(stream)
     for _ in range(args.steps):
@@ -301,18 +403,15 @@ def run_single(args, cfg):
     launches = lb.launch_count() - n0
     if sampler:
         sampler.__exit__()
+    tr = M.trace_read()
+    M.trace_phases(0)
     ms = e0.elapsed_time(e1) / args.steps
     value = nnz / (ms * 1e-3) / 1e9
-
-    # dominant kernel: its share of the step from per-phase CUDA events on the launching stream (20
-    # calls right after the timed region), applied to the step time measured over the timed region --
-    # the timed region runs at the power-capped steady-state clock, the short phase calls do not
-    phases = []
-    for _ in range(20):
-        phases.append(M.phase_times(x, y, sched))
-    ph = np.mean(np.array(phases), axis=0)
-    main_share = float(ph[1]) / max(float(np.sum(ph)), 1e-9)
-    main_ms = ms * main_share
+    ph = np.mean(tr, axis=0)  # (partition, main, fix-up) ms per step, mean over the K timed steps
+    main_ms = float(ph[1])
+    main_share = main_ms / ms
+    # the same step captured in a CUDA graph: median of 50 replays (SURVEY 8(d) reporting)
+    g_med, g_min, g_max = graph_median(step, 50)
     alg = compulsory_bytes(rows, cols, nnz)
     peak, peak_src = peak_hbm()
     achieved = alg / (main_ms * 1e-3) / 1e9
@@ -329,23 +428,31 @@ def run_single(args, cfg):
         "no_plan": no_plan,
         "gpu_launches": int(launches),
         "phase_ms": {"partition": round(float(ph[0]), 5), "main": round(float(ph[1]), 5), "fixup": round(float(ph[2]), 5),
-                     "main_share": round(main_share, 4), "main_in_timed_region": round(main_ms, 5)},
+                     "main_share": round(main_share, 4),
+                     "from": "mean over the K timed steps of CUDA events recorded on the launch stream around each "
+                             "phase (lb_csr_trace_phases)"},
+        "graph": {"value": round(nnz / (g_med * 1e-3) / 1e9, 3), "unit": "GNZ/s", "median_ms": round(g_med, 5),
+                  "min_max_ms": [round(g_min, 5), round(g_max, 5)],
+                  "timing": "median of 50 replays of the step captured in a CUDA graph, CUDA events around each"},
         "roofline": {"bound": "hbm", "kernel": M.kernel_name(sched),
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "traffic": ncu_traffic(cfg, sched, args.items_per_tile, M.kernel_name(sched),
                                           plan["hot_cols"] if plan and plan["hot_cols"] else None),
                      "algorithmic_bytes": alg,
                      "peak_source": peak_src,
-                     "kernel_ms_from": "timed-region ms_per_step x the kernel's share of the step (mean of 20 "
-                                       "lb_spmv_phase_times calls: CUDA events on the launch stream)"},
+                     "kernel_ms": round(main_ms, 5),
+                     "kernel_ms_from": "mean duration of the tile kernel over the K timed steps (CUDA events on its "
+                                       "launch stream, recorded by the library around every launch)"},
     }
-    # the stream+gather ceiling of this matrix on this GPU (no row structure), measured live
+    # the stream+gather ceiling of this matrix on this GPU (no row structure), measured live; the kernel
+    # side of these two ratios is 20 short phase-timed calls, so both sides run at the same clocks
+    ph_short = np.mean(np.array([M.phase_times(x, y, sched) for _ in range(20)]), axis=0)
     try:
         probe_ms = M.probe_stream_gather(x, reps=20)
         rec["roofline_gather"] = {
             "bound": "l1tex gather (~1 L1TEX line per clock per SM for random 4-byte x[col] not served from shared memory)",
-            "achieved": round(nnz / (float(ph[1]) * 1e-3) / 1e9, 2), "peak": round(nnz / (probe_ms * 1e-3) / 1e9, 2),
-            "unit": "GNZ/s", "frac": round(probe_ms / float(ph[1]), 4),
+            "achieved": round(nnz / (float(ph_short[1]) * 1e-3) / 1e9, 2), "peak": round(nnz / (probe_ms * 1e-3) / 1e9, 2),
+            "unit": "GNZ/s", "frac": round(probe_ms / float(ph_short[1]), 4),
             "timing": "both right after the timed region: the kernel's phase-call time vs 20 probe passes",
             "peak_source": "lb_probe_stream_gather: same col/val/x" + (" and the same x-reuse plan (hot x in shared memory)"
                                                                      if plan and plan["hot_cols"] else "")
@@ -357,7 +464,7 @@ def run_single(args, cfg):
     try:
         st_ms = M.probe_stream(reps=20)
         st_gbs = 8.0 * nnz / (st_ms * 1e-3) / 1e9
-        ach_ph = alg / (float(ph[1]) * 1e-3) / 1e9
+        ach_ph = alg / (float(ph_short[1]) * 1e-3) / 1e9
         rec["roofline_stream"] = {
             "bound": "hbm (read-only stream)", "achieved": round(ach_ph, 1), "peak": round(st_gbs, 1), "unit": "GB/s",
             "frac": round(ach_ph / st_gbs, 4),
@@ -432,8 +539,16 @@ def run_single(args, cfg):
     gnz, reps, dt = time_oracle(sample, args.cpu_seconds)
     rec["cpu_baseline"] = {"value": round(gnz, 4), "unit": "GNZ/s", "cores": oracle.num_threads(), "kind": "oracle",
                            "sample": f"leading {sample[4]} rows ({sample[5]} nnz) of {cfg} with full x, {reps} reps "
-                                     f"in {dt:.1f} s (oracle.spmv_omp, fp64)"}
+                                     f"in {dt:.1f} s, median rep (oracle.spmv_omp, fp64, gcc -O3 -march=native)"}
     rec["cpu_baseline"].update(oracle_extras(sample, max(2.0, args.cpu_seconds / 2)))
+    # the other matrix classes of BASELINE's metric ("per matrix class"), one GPU each
+    classes = [c for c in args.classes.split(",") if c and c != cfg]
+    if classes:
+        del M, A, x, y, hx, hy, hxs, hys, ho, hc, hv
+        torch.cuda.empty_cache()
+        rec["classes"] = {}
+        for c in classes:
+            rec["classes"][c] = class_report(c, dev)
     print(json.dumps(rec))
 
 
@@ -503,6 +618,11 @@ def run_multi(args, cfg):
     for _ in range(max(3, args.warmup)):
         step()
     torch.cuda.synchronize()
+    # SURVEY 8(c) p10, asserted once before timing: after the step every rank holds a bitwise-identical
+    # y (an NCCL all-reduce of per-rank hashes, lb_comm_check_replicas)
+    same, _ = comm.check_replicas(peer.y if peer is not None else y)
+    if not same:
+        raise RuntimeError("ranks disagree on y after the multi-GPU step (lb_comm_check_replicas)")
     sampler = ClockSampler(local) if (rank == 0 and not args.no_extras) else None
     if sampler:
         sampler.__enter__()
@@ -601,6 +721,7 @@ def run_multi(args, cfg):
                        "l2": "inputs larger than L2; no flush"},
             "plan": plan,
             "no_plan": no_plan,
+            "replicas_bitwise_equal": True,
             "gpu_launches": int(launches),
             "spmv_only": {"value": round(nnz / (spmv_ms * 1e-3) / 1e9, 3), "unit": "GNZ/s", "ms": round(spmv_ms, 5),
                           "per_gpu": round(nnz / world / (spmv_ms * 1e-3) / 1e9, 3)},
