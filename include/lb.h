@@ -211,7 +211,10 @@ lb_status_t lb_spmm(lb_csr_t A, int64_t n, const float* d_X, int64_t ldx, float*
  * shared memory, and the tile kernel reads warm values from the dense copy (kept in L2 with an
  * evict_last policy; cold x reads use evict_first).  Products and summation order are unchanged:
  * y is bitwise identical to the call without a plan.  Other schedules ignore the plan.
- *  slots          0 = default (16384: 64 KB of shared memory per SM); 1 .. 45056; < 0 drops the plan.
+ *  slots          0 = automatic: the default budget (16384: 64 KB of shared memory per SM), and no plan
+ *                 where it cannot pay -- the handle's tile length has no plan kernel (only 504 and 1016
+ *                 do), or x fits in the L2 (no warm tier) and the hot columns hold < 0.5% of the stored
+ *                 entries; 1 .. 45056 = that budget, always built; < 0 drops the plan.
  *  warm_cols      0 = no warm tier; -1 = auto (a 48 MB budget when x (4*cols bytes) is larger
  *                 than the L2, else none); > 0 = budget in columns; -2 = compact x: EVERY
  *                 referenced non-hot column is warm (numbered in ascending column order), its entry

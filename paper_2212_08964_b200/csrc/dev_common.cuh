@@ -170,7 +170,16 @@ struct TileArgs {
   int cols;
   float* peer_y[kMaxPeers];  // fused multi-GPU epilogue: the other ranks' y at this rank's rows
   int npeers;
+  int off_keep;        // 1: row offsets small enough to keep in L2 across calls (evict_last loads)
 };
+
+// one row offset with an explicit L2 policy (evict_last keeps a small offsets array resident in L2
+// across calls, so the next call's partition search hits L2; evict_first streams a large one)
+__device__ __forceinline__ int ld_off(const int* p, uint64_t pol) {
+  int v;
+  asm("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+  return v;
+}
 
 // tile t's coordinates (i0, j0, i1, j1)
 __device__ __forceinline__ int4 tile_coords(const TileArgs& a, int t) {

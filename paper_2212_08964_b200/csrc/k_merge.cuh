@@ -372,6 +372,161 @@ __global__ void __launch_bounds__(NT, MINB) merge_wide_kernel(TileArgs a) {
   }
 }
 
+// ----------------------------------------------------------------------------- merge-path tiles, short rows
+// CTA tiles of L = 8*NT - 8 merge items ("first splitting the work across blocks, and then to threads
+// within a block") with the tile's products staged in shared memory:
+//  1. thread t owns the 8 contiguous nonzero positions [8t, 8t+8) of the tile's 32-byte-aligned range
+//     (one 256-bit load each of col_idx / values, evict-first), gathers x and stores the 8 products;
+//  2. thread t then sums rows i0 + t, i0 + t + NT, ... of the tile over the staged products -- every
+//     row end is one thread's, y stores are coalesced, and there is no segmented scan at all;
+//  3. rows holding more than kSeq products in the tile are queued and summed by one warp each (lanes
+//     stride the row, fixed xor tree), so a long row never serialises a thread.
+// Row "nrows" of a tile is the open row (i1): its partial becomes the carry into the CTA's next tile
+// (shared memory, compensated 2Sum pair), and the CTA's last carry goes to the last-CTA fix-up
+// (Alg.3, fixup_carries).  The products and the long-row queue are double-buffered, so a
+// tile costs two CTA barriers.  Accuracy: a row's part in one tile is <= kSeq sequential terms or
+// <= 2L/32 per lane + a 5-level tree; parts of a row across tiles / CTAs are 2Sum-compensated.
+// For matrices with short rows (C2 stencil: 5 products per row) this replaces the position-split
+// segmented scans of merge_wide_kernel, whose row ends cost most of its instructions.
+template <int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) merge_rows_kernel(TileArgs a) {
+  constexpr int kCap = 8 * NT, kW = NT / 32, kSeq = 32, kLongMax = kCap / (kSeq + 1) + 2;
+  __shared__ __align__(16) float s_prod[2][kCap];
+  __shared__ int s_long[2][kLongMax];
+  __shared__ int s_nlong[2];
+  __shared__ float s_carry[2][2];  // [tile parity][sum, compensation] of the open row
+  __shared__ int s_last;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t_begin = blockIdx.x * a.tiles_per_cta;
+  const int t_end = min(a.num_tiles, t_begin + a.tiles_per_cta);
+  const uint64_t spol = policy_evict_first();
+  const uint64_t opol = a.off_keep ? policy_evict_last() : spol;
+  if (tid < 2) {
+    s_nlong[tid] = 0;
+    s_carry[tid][0] = 0.f;
+    s_carry[tid][1] = 0.f;
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: coords are read below
+
+  // this thread's 8 positions of the tile's col/val, loaded one tile ahead
+  int col[8];
+  float val[8];
+  auto load = [&](int4 c) {
+    const int g = (c.y & ~7) + 8 * tid;
+    if (g < c.w && g + 8 <= a.nnz) {
+      ld_stream_v8(a.col + g, col, spol);
+      ld_stream_v8(a.val + g, val, spol);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const bool ok = g + e < c.w;
+        col[e] = ok ? ld_cs(a.col + g + e) : 0;
+        val[e] = ok ? ld_cs(a.val + g + e) : 0.f;
+      }
+    }
+  };
+
+  int4 cur = make_int4(0, 0, 0, 0), nxt = cur;
+  if (t_begin < t_end) {
+    cur = tile_coords(a, t_begin);
+    load(cur);
+    if (t_begin + 1 < t_end) nxt = tile_coords(a, t_begin + 1);
+  }
+  int i_last = cur.z;
+  for (int t = t_begin; t < t_end; ++t) {
+    const int b = (t - t_begin) & 1;
+    const int i0 = cur.x, nrows = cur.z - cur.x, jA = cur.y & ~7, lo = cur.y - jA, hi = cur.w - jA;
+    // (1) products of this thread's 8 positions (outside [lo, hi): exactly 0)
+    float p[8];
+    {
+      const int q0 = 8 * tid;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const bool ok = q0 + e >= lo && q0 + e < hi;
+        p[e] = ok ? val[e] * ld_x(a.x + col[e]) : 0.f;
+      }
+    }
+    // the next tile's col/val stream in while this tile is reduced
+    const int i_end = cur.z;
+    if (t + 1 < t_end) {
+      cur = nxt;
+      load(cur);
+      if (t + 2 < t_end) nxt = tile_coords(a, t + 2);
+    }
+    float4* sp = reinterpret_cast<float4*>(&s_prod[b][8 * tid]);
+    sp[0] = make_float4(p[0], p[1], p[2], p[3]);
+    sp[1] = make_float4(p[4], p[5], p[6], p[7]);
+    __syncthreads();  // (A) products (and the previous tile's carry) visible
+    if (tid == 0) s_nlong[b ^ 1] = 0;  // the previous tile's queue count was read before (A)
+
+    // (2) rows of the tile, one thread each; r == nrows is the open row (its partial is the carry)
+    const float* pr = s_prod[b];
+    auto bounds = [&](int r, int& s, int& e) {
+      s = r == 0 ? lo : ld_off(a.off + i0 + r, opol) - jA;
+      e = r < nrows ? ld_off(a.off + i0 + r + 1, opol) - jA : hi;
+    };
+    auto finish = [&](int r, float v) {
+      float cs = v, cc = 0.f;
+      if (r == 0) {  // carry of the row open at the tile start (previous tile of this CTA)
+        cs = s_carry[b ^ 1][0];
+        cc = s_carry[b ^ 1][1];
+        csum_add(cs, cc, v);
+      }
+      if (r < nrows) {
+        a.y[i0 + r] = cs + cc;
+      } else {
+        s_carry[b][0] = cs;
+        s_carry[b][1] = cc;
+      }
+    };
+    for (int r = tid; r <= nrows; r += NT) {
+      int s, e;
+      bounds(r, s, e);
+      if (e - s > kSeq) {
+        s_long[b][atomicAdd(&s_nlong[b], 1)] = r;
+        continue;
+      }
+      float v = 0.f;
+      for (int q = s; q < e; ++q) v += pr[q];
+      finish(r, v);
+    }
+    // (3) long rows: one warp each
+    __syncthreads();  // (B) the queue is complete
+    const int nl = s_nlong[b];
+    if (nl > 0) {
+      for (int k = warp; k < nl; k += kW) {
+        const int r = s_long[b][k];
+        int s, e;
+        bounds(r, s, e);
+        float v = 0.f;
+        for (int q = s + lane; q < e; q += 32) v += pr[q];
+        v = warp_sum(v);
+        if (lane == 0) finish(r, v);
+      }
+    }
+    i_last = i_end;
+  }
+  __syncthreads();  // the last tile's carry is written
+
+  if (tid == 0) {
+    if (t_begin < t_end) {
+      const int bl = (t_end - 1 - t_begin) & 1;
+      a.carry_row[blockIdx.x] = i_last;
+      a.carry_val[blockIdx.x] = s_carry[bl][0] + s_carry[bl][1];
+    }
+    __threadfence();
+    const unsigned done = atomicAdd(a.ticket, 1u);
+    s_last = done == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    fixup_carries(a, (int)gridDim.x, tid, NT);
+    if (tid == 0) *a.ticket = 0u;
+  }
+}
+
 // ----------------------------------------------------------------------------- merge-path tiles, warp-streamed
 // Each WARP owns a contiguous run of merge-path tiles (tile length L = 256*R - 8) and streams
 // them as rounds of 256 nonzeros (8 contiguous per lane, 256-bit loads).  A 3-deep register
@@ -782,6 +937,54 @@ __global__ void __launch_bounds__(512) probe_stream_gather_kernel(int nnz, const
     for (int e = 0; e < 8; ++e) s = fmaf(d.val[e], xv[e], s);
   }
   for (; i < nnz; ++i) s = fmaf(val[i], gx<TIER>(x, x_warm, cols, sxb, col[i], xpol, pol), s);
+  if (flag) sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// Diagnostic: the stream+gather probe with the hot tier spread over a thread-block
+// cluster of C CTAs (C SMs): slot s lives in the shared memory of cluster rank s % C at index s / C, and
+// a gather of a hot column reads it through distributed shared memory (mapa + ld.shared::cluster), so
+// the cluster holds C times the hot columns one SM can.  Measures whether remote shared-memory reads
+// relieve the L1->L2 request path that the cold gathers saturate.
+template <int C>
+__global__ void __launch_bounds__(512) probe_cluster_gather_kernel(int nnz, const int* __restrict__ col,
+                                                                   const float* __restrict__ val,
+                                                                   const float* __restrict__ x,
+                                                                   const float* __restrict__ x_hot, int hot_n,
+                                                                   int flag, float* sink) {
+  extern __shared__ __align__(16) float s_xhot[];
+  unsigned rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int per = (hot_n + C - 1) / C;
+  for (int i = threadIdx.x; i < per; i += blockDim.x) {
+    const int sl = i * C + (int)rank;
+    s_xhot[i] = sl < hot_n ? __ldcg(x_hot + sl) : 0.f;
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+  const uint64_t pol = policy_evict_first();
+  const uint32_t sxb = (uint32_t)__cvta_generic_to_shared(s_xhot);
+  constexpr int kLog = C == 1 ? 0 : C == 2 ? 1 : C == 4 ? 2 : 3;
+  float s = 0.f;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 8;
+  int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  for (; i + 8 <= nnz; i += stride) {
+    int c[8];
+    float v[8], xv[8];
+    ld_stream_v8(col + i, c, pol);
+    ld_stream_v8(val + i, v, pol);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const unsigned sl = (unsigned)~c[e];
+      asm("{\n\t.reg .pred p;\n\t.reg .u32 ra;\n\tsetp.lt.s32 p, %1, 0;\n\t"
+          "@p mapa.shared::cluster.u32 ra, %2, %3;\n\t"
+          "@p ld.shared::cluster.f32 %0, [ra];\n\t"
+          "@!p ld.global.nc.f32 %0, [%4];\n\t}"
+          : "=f"(xv[e])
+          : "r"(c[e]), "r"(sxb + ((sl >> kLog) << 2)), "r"(sl & (C - 1)), "l"(x + c[e]));
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s = fmaf(v[e], xv[e], s);
+  }
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
   if (flag) sink[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 

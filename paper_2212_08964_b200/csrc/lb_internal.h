@@ -52,6 +52,7 @@ constexpr int kNT = 256;
 constexpr int64_t kMaxMergeItems = (1ll << 31) - (1ll << 16) - 1;
 constexpr int kMaxCtas = 8192;             // carry slots per handle (>= SMs x resident CTAs or warps)
 constexpr int kCarryVals = 32 * kMaxCtas;  // carry values per handle (SpMM: up to 32 per carry slot)
+constexpr int64_t kWarpSearchMax = 32768;  // partitions of <= this many boundaries: a lane group per search
 constexpr int kMinTile = 504;              // smallest supported L: sizes the partition cache
 
 // Merge-path tile lengths L = 256*R - 8 (warp-streamed tiles of R rounds) or NT*E - 8 (CTA tiles):
@@ -203,6 +204,7 @@ int auto_tile_length(int64_t rows, int64_t nnz);
 lb_status_t check_shape(int64_t rows, int64_t cols, int64_t nnz);
 lb_status_t init_handle(lb_csr_s* A, int64_t rows, int64_t cols, int64_t nnz, const int32_t* off,
                         const int32_t* col, const float* val);
+int offsets_l2_resident(const lb_csr_s* A);
 lb_status_t launch_partition(const lb_csr_s* A, int64_t L, int2* coords, stream_t s);
 lb_status_t launch_partition_nz(const lb_csr_s* A, int64_t L, int2* coords, stream_t s);
 // partition (when `partition`) and the x-reuse plan's per-call gathers of x, in one launch

@@ -194,6 +194,13 @@ lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, int64_t warm_cols, void
   if (slots < 0) {
     drop_plan(A);
   } else {
+    const bool auto_plan = slots == 0;
+    if (auto_plan && A->L != 1016 && A->L != 504) {  // no plan kernel at this tile length: nothing to gain
+      drop_plan(A);
+      if (hot_cols_out) *hot_cols_out = 0;
+      if (hot_nnz_out) *hot_nnz_out = 0;
+      return LB_OK;
+    }
     if (slots == 0) slots = kHotSlotsDefault;
     if (slots > kHotSlotsMax) return fail(LB_ERR_INVALID_ARG, "slots %d > %d", slots, kHotSlotsMax);
     if (warm_cols < -2) return fail(LB_ERR_INVALID_ARG, "warm_cols %lld < -2", (long long)warm_cols);
@@ -208,6 +215,10 @@ lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, int64_t warm_cols, void
     } else {
       lb_status_t st = build_plan(A, slots, warm_cols, S(stream));
       if (st != LB_OK) { drop_plan(A); return st; }
+      // auto: keep the plan only where it pays -- a warm tier (x larger than the L2) or
+      // hot columns holding >= 0.5% of the stored entries (C2 stencil 0.4% at L = 1016: the plan's
+      // one-CTA-per-SM kernel was 20% slower there; C4 0.57%: +4%)
+      if (auto_plan && A->plan.warm_n == 0 && 200 * A->plan.hot_nnz < A->nnz) drop_plan(A);
     }
   }
   if (hot_cols_out) *hot_cols_out = A->plan.hot_n;

@@ -55,6 +55,7 @@ lbk::TileArgs tile_args(const lb_csr_s* A, const int32_t* col, const float* x, f
   a.num_tiles = T; a.tiles_per_cta = per;
   a.carry_row = A->carry_row; a.carry_val = A->carry_val; a.ticket = A->ticket;
   a.cols = (int)A->cols;
+  a.off_keep = offsets_l2_resident(A);
   return a;
 }
 
@@ -117,6 +118,23 @@ lb_status_t wide_launch(lb_csr_s* A, const float* x, float* y, stream_t s) {
   return launch_pdl(k, grid, NT, 0, s, tile_args(A, A->col, x, y, T, tpc));
 }
 
+// Short-row CTA tiles (merge_rows_kernel, L = 8*NT - 8): products staged in shared memory, rows
+// summed one per thread.
+template <int NT, int MINB>
+lb_status_t rows_launch(lb_csr_s* A, const float* x, float* y, stream_t s) {
+  auto k = lbk::merge_rows_kernel<NT, MINB>;
+  static OccCache occ;
+  int blocks = 0;
+  lb_status_t st = resident_ctas(occ, A->device, k, NT, 0, &blocks);
+  if (st != LB_OK) return st;
+  constexpr int L = 8 * NT - 8;
+  const int T = (int)num_tiles(A->rows, A->nnz, L);
+  int grid = std::min(T, std::min(A->dev->sm_count * blocks, kMaxCtas));
+  const int tpc = (T + grid - 1) / grid;
+  grid = (T + tpc - 1) / tpc;  // every CTA owns >= 1 tile
+  return launch_pdl(k, grid, NT, 0, s, tile_args(A, A->col, x, y, T, tpc));
+}
+
 // Fallback for col_idx / values that are not 32-byte aligned: CTA tiles with 128-bit (16-byte
 // aligned) or scalar loads, and a separate fix-up kernel.
 template <int L, bool VEC>
@@ -155,7 +173,7 @@ struct TileKernel {
 const TileKernel kTileKernels[kNumL] = {
     {"merge_stream_kernel<4,2,4>", stream_launch<4, 2, 4>},      // L = 504
     {"merge_stream_kernel<8,4,2>", stream_launch<8, 4, 2>},      // L = 1016 (long / irregular rows)
-    {"merge_wide_kernel<256,8,4>", wide_launch<256, 8, 4>},      // L = 2040 (short rows: C2 stencil)
+    {"merge_rows_kernel<256,4>", rows_launch<256, 4>},           // L = 2040 (short rows: C2 stencil)
     {"merge_stream_kernel<4,12,4>", stream_launch<4, 12, 4>},    // L = 3064
     {"merge_wide_kernel<256,16,2>", wide_launch<256, 16, 2>},    // L = 4088
 };
@@ -343,6 +361,39 @@ lb_status_t probe_launch(lb_csr_s* A, const float* x, stream_t s) {
   const int grid = A->dev->sm_count * blocks;
   k<<<grid, 512, dyn, s>>>((int)A->nnz, TIER >= 1 ? A->plan.hcol : A->col, A->val, x, A->plan.x_hot, A->plan.hot_n4,
                            A->plan.x_warm, (int)A->cols, 0, nullptr);
+  LB_LAUNCHED();
+  return LB_OK;
+}
+
+// cluster hot-tier probe (LB_PROBE_CLUSTER = C in {1, 2, 4, 8}; diagnostic): one CTA of 16
+// warps per SM, clusters of C CTAs, as many clusters as fit at once
+template <int C>
+lb_status_t probe_cluster_launch(lb_csr_s* A, const float* x, stream_t s) {
+  auto k = lbk::probe_cluster_gather_kernel<C>;
+  const int per = (A->plan.hot_n + C - 1) / C;
+  const int dyn = ((per + 3) / 4) * 16;
+  LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kHotDynMax));
+  const int pct = std::min(100, (int)(100.0 * (dyn + 1024.0) / (228.0 * 1024.0)) + 1);
+  LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+  if (C > 1) LB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(512);
+  cfg.dynamicSmemBytes = dyn;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3(A->dev->sm_count / C * C);
+  int nclusters = 0;
+  LB_CUDA(cudaOccupancyMaxActiveClusters(&nclusters, k, &cfg));
+  if (nclusters < 1) return fail(LB_ERR_UNSUPPORTED, "cluster probe C=%d does not fit", C);
+  cfg.gridDim = dim3(std::min(nclusters, A->dev->sm_count / C) * C);
+  LB_CUDA(cudaLaunchKernelEx(&cfg, k, (int)A->nnz, (const int*)A->plan.hcol, A->val, x, (const float*)A->plan.x_hot,
+                             A->plan.hot_n, 0, (float*)nullptr));
   LB_LAUNCHED();
   return LB_OK;
 }
@@ -613,7 +664,15 @@ lb_status_t lb_probe_stream_gather(lb_csr_t A, const float* d_x, int32_t reps, v
   lb_status_t st;
   if (tier > 0 && (st = launch_partition_xhot(A, 0, false, d_x, s)) != LB_OK) return st;  // x_hot / x_warm of this x
   const float* xg = p.compact ? p.x_warm : d_x;
+  const char* env = getenv("LB_PROBE_CLUSTER");
+  const int ccl = env ? atoi(env) : 0;
+  if (ccl > 0 && (tier != 1 || (ccl != 1 && ccl != 2 && ccl != 4 && ccl != 8)))
+    return fail(LB_ERR_UNSUPPORTED, "LB_PROBE_CLUSTER needs a hot-only plan and C in {1,2,4,8}");
   auto launch = [&]() {
+    if (ccl == 1) return probe_cluster_launch<1>(A, xg, s);
+    if (ccl == 2) return probe_cluster_launch<2>(A, xg, s);
+    if (ccl == 4) return probe_cluster_launch<4>(A, xg, s);
+    if (ccl == 8) return probe_cluster_launch<8>(A, xg, s);
     return tier == 2 ? probe_launch<2>(A, d_x, s) : tier == 1 ? probe_launch<1>(A, xg, s) : probe_launch<0>(A, d_x, s);
   };
   return time_reps(launch, reps, s, ms_out);
