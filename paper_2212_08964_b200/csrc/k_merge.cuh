@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(NT, MINB) merge_wide_kernel(TileArgs a) {
   __syncthreads();
   if (s_last) {
     __threadfence();
-    fixup_carries(a, (int)gridDim.x, tid, NT);
+    fixup_carries_blocked(a, (int)gridDim.x, tid, NT);
     if (tid == 0) *a.ticket = 0u;
   }
 }
@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(NT, MINB) merge_rows_kernel(TileArgs a) {
   __syncthreads();
   if (s_last) {
     __threadfence();
-    fixup_carries(a, (int)gridDim.x, tid, NT);
+    fixup_carries_blocked(a, (int)gridDim.x, tid, NT);
     if (tid == 0) *a.ticket = 0u;
   }
 }
@@ -788,15 +788,8 @@ __device__ __forceinline__ void stream_carries_fixup(const TileArgs& a, int gw, 
   __syncthreads();
   if (s_last) {
     __threadfence();
-    const int nc = (int)gridDim.x * W;
-    for (int c = threadIdx.x; c < nc; c += W * 32) {
-      const int r = __ldcg(a.carry_row + c);
-      if (r >= a.rows) continue;
-      if (c > 0 && __ldcg(a.carry_row + c - 1) == r) continue;
-      float sum = __ldcg(a.y + r), comp = 0.f;
-      for (int kk = c; kk < nc && __ldcg(a.carry_row + kk) == r; ++kk) csum_add(sum, comp, __ldcg(a.carry_val + kk));
-      put_y<PEERS>(a, r, sum + comp);
-    }
+    fixup_carries_blocked(a, (int)gridDim.x * W, threadIdx.x, W * 32,
+                          [&](int r, float v) { put_y<PEERS>(a, r, v); });
     if (threadIdx.x == 0) *a.ticket = 0u;
     if (PEERS) __threadfence_system();
   }

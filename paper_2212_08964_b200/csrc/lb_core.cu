@@ -288,6 +288,7 @@ lb_status_t lb_partition_size(lb_csr_t A, int32_t items_per_tile, int64_t* n) {
 }
 
 lb_status_t lb_partition(lb_csr_t A, int32_t items_per_tile, int32_t* d_coords, void* stream) {
+  LB_NVTX("lb_partition");
   g_err.clear();
   if (!A || !d_coords) return fail(LB_ERR_INVALID_ARG, "null argument");
   int64_t L = items_per_tile == 0 ? A->L : items_per_tile;

@@ -121,6 +121,7 @@ extern "C" {
 
 lb_status_t lb_spmv_host_x(lb_csr_t A, lb_schedule_t sched, const float* h_x, float* h_y, uint32_t flags,
                            void* stream) {
+  LB_NVTX("lb_spmv_host_x");
   g_err.clear();
   if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
   if (A->rows == 0) return LB_OK;
@@ -150,6 +151,7 @@ lb_status_t lb_spmv_host_x(lb_csr_t A, lb_schedule_t sched, const float* h_x, fl
 
 lb_status_t lb_spmv_host_x_async(lb_csr_t A, lb_schedule_t sched, const float* h_x, float* h_y, uint32_t flags,
                                  void* stream) {
+  LB_NVTX("lb_spmv_host_x_async");
   g_err.clear();
   if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
   if (A->rows == 0) return LB_OK;
@@ -194,6 +196,7 @@ lb_status_t lb_spmv_host_x_async(lb_csr_t A, lb_schedule_t sched, const float* h
 }
 
 lb_status_t lb_spmv_host_x_wait(lb_csr_t A) {
+  LB_NVTX("lb_spmv_host_x_wait");
   g_err.clear();
   if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
   if (!A->host.mem) return LB_OK;
@@ -211,6 +214,7 @@ size_t lb_spmv_host_workspace_size(int64_t rows, int64_t cols, int64_t nnz) {
 lb_status_t lb_spmv_host(int64_t rows, int64_t cols, int64_t nnz, const int32_t* h_row_offsets,
                          const int32_t* h_col_idx, const float* h_values, const float* h_x, float* h_y,
                          lb_schedule_t sched, void* d_workspace, size_t workspace_bytes, void* stream) {
+  LB_NVTX("lb_spmv_host");
   g_err.clear();
   lb_status_t st = check_shape(rows, cols, nnz);
   if (st != LB_OK) return st;

@@ -21,7 +21,20 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace lbi {
+
+// NVTX ranges around the public entry points (compute / exchange overlap is read off an nsys
+// timeline); header-only NVTX v3, a no-op unless a tool injects itself.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define LB_NVTX(name) ::lbi::NvtxRange lb_nvtx_range_(name)
+
 
 using stream_t = cudaStream_t;
 inline stream_t S(void* s) { return reinterpret_cast<stream_t>(s); }

@@ -347,6 +347,7 @@ lb_status_t lb_comm_check_replicas(lb_comm_t c, const float* d_y, int64_t n, voi
 }
 
 lb_status_t lb_allgather_rows(lb_comm_t c, const int64_t* h_bounds, float* d_y_full, void* stream) {
+  LB_NVTX("lb_allgather_rows");
   g_err.clear();
   if (!c || !h_bounds || !d_y_full) return fail(LB_ERR_INVALID_ARG, "null argument");
   std::vector<int64_t> off(c->nranks), cnt(c->nranks);
@@ -359,6 +360,7 @@ lb_status_t lb_allgather_rows(lb_comm_t c, const int64_t* h_bounds, float* d_y_f
 }
 
 lb_status_t lb_allgather_padded(lb_comm_t c, int64_t padded_rows, float* d_y_pad, void* stream) {
+  LB_NVTX("lb_allgather_padded");
   g_err.clear();
   if (!c || !d_y_pad || padded_rows < 0) return fail(LB_ERR_INVALID_ARG, "bad padded all-gather arguments");
   if (padded_rows == 0) return LB_OK;
@@ -436,6 +438,7 @@ lb_status_t lb_peer_destroy(lb_peer_t p) {
 
 lb_status_t lb_spmv_multi_fused(lb_csr_t A_local, lb_peer_t peer, lb_schedule_t sched, const int64_t* h_bounds,
                                 const float* d_x_full, uint32_t flags, void* stream) {
+  LB_NVTX("lb_spmv_multi_fused");
   g_err.clear();
   if (!A_local || !peer || !h_bounds || !d_x_full) return fail(LB_ERR_INVALID_ARG, "null argument");
   lb_comm_s* c = peer->comm;
@@ -564,6 +567,7 @@ lb_status_t lb_spmv_multi(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, co
 
 lb_status_t lb_spmv_multi_ex(lb_csr_t A_local, lb_comm_t c, lb_schedule_t sched, const int64_t* h_bounds,
                              const float* d_x_full, float* d_y_full, uint32_t flags, void* stream) {
+  LB_NVTX("lb_spmv_multi_ex");
   g_err.clear();
   if (!A_local || !c || !h_bounds || !d_x_full || !d_y_full) return fail(LB_ERR_INVALID_ARG, "null argument");
   if ((const void*)d_x_full == (const void*)d_y_full) return fail(LB_ERR_INVALID_ARG, "x and y must not alias");

@@ -189,6 +189,7 @@ extern "C" {
 
 lb_status_t lb_csr_plan_hot_x(lb_csr_t A, int32_t slots, int64_t warm_cols, void* stream, int32_t* hot_cols_out,
                               int64_t* hot_nnz_out) {
+  LB_NVTX("lb_csr_plan_hot_x");
   g_err.clear();
   if (!A) return fail(LB_ERR_INVALID_ARG, "null handle");
   if (slots < 0) {

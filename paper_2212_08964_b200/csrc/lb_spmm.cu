@@ -144,6 +144,7 @@ using namespace lbi;
 extern "C" {
 
 lb_status_t lb_spmm(lb_csr_t A, int64_t n, const float* d_X, int64_t ldx, float* d_Y, int64_t ldy, void* stream) {
+  LB_NVTX("lb_spmm");
   g_err.clear();
   return spmm_impl(A, n, d_X, ldx, d_Y, ldy, S(stream));
 }

@@ -553,11 +553,13 @@ using namespace lbi;
 extern "C" {
 
 lb_status_t lb_spmv(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_y, void* stream) {
+  LB_NVTX("lb_spmv");
   g_err.clear();
   return spmv_impl(A, sched, d_x, d_y, 0u, S(stream), nullptr);
 }
 
 lb_status_t lb_spmv_ex(lb_csr_t A, lb_schedule_t sched, const float* d_x, float* d_y, uint32_t flags, void* stream) {
+  LB_NVTX("lb_spmv_ex");
   g_err.clear();
   return spmv_impl(A, sched, d_x, d_y, flags, S(stream), nullptr);
 }

@@ -101,6 +101,7 @@ using namespace lbi;
 extern "C" {
 
 lb_status_t lb_sssp(lb_csr_t A, int64_t source, lb_schedule_t sched, float* d_dist, void* stream, int32_t* rounds_out) {
+  LB_NVTX("lb_sssp");
   g_err.clear();
   return sssp_impl(A, source, sched, d_dist, S(stream), rounds_out);
 }

@@ -14,8 +14,8 @@ for cfg in cfgs:
     x = lbgen.x_for_config(cfg, A.cols, "float", device="cuda")
     M = lb.CsrMatrix.from_csr(A)
     y = torch.empty(A.rows, device="cuda")
-    M.set_items_per_tile(1016 if os.environ.get("LB_ROWS_VARIANT", "0") in ("4", "5") else 2040)
-    out = {"config": cfg, "variant": os.environ.get("LB_ROWS_VARIANT", "0"), "kernel": M.kernel_name("merge_path")}
+    M.set_items_per_tile(1016 if False else 2040)
+    out = {"config": cfg, "variant": os.environ.get("LB_SHORT_KERNEL", "0"), "kernel": M.kernel_name("merge_path")}
     for sched in ("merge_path", "thread_mapped"):
         med, lo, hi = graph_median(lambda: M.spmv(x, y, sched, repartition=True), 50)
         ph = np.mean(np.array([M.phase_times(x, y, sched) for _ in range(20)]), axis=0)
