@@ -320,12 +320,12 @@ lb_status_t lb_spmv_host_x(lb_csr_t A, lb_schedule_t sched, const float* h_x, fl
 /*
  * lb_spmv_host_x_async / lb_spmv_host_x_wait -- the same y = A x with HOST x and y as lb_spmv_host_x,
  * for a stream of independent right-hand sides (many x vectors against one resident matrix, e.g. a
- * serving batch): the call only ENQUEUES the pinned H2D copy of h_x [cols] into one of two staging
+ * serving batch): the call only ENQUEUES the pinned H2D copy of h_x [cols] into one of three staging
  * slots the handle owns (on an H2D stream of its own), the SpMV of `sched` with `flags` on `stream`
  * (as lb_spmv_ex; it waits for that copy) and the D2H copy of y [rows] into h_y (on a D2H stream of
- * its own, after the SpMV), and returns.  Consecutive calls alternate the two slots, so call k's
+ * its own, after the SpMV), and returns.  Consecutive calls rotate through the slots, so call k's
  * H2D, call k-1's SpMV and call k-2's D2H can run at once (PCIe is full duplex); a call reuses a slot
- * only after the SpMV and the D2H of the call two back on it (stream-ordered event waits, no host
+ * only after the SpMV and the D2H of the call three back on it (stream-ordered event waits, no host
  * sync).  Ownership: h_x must stay unmodified and h_y untouched until lb_spmv_host_x_wait returns;
  * h_y holds y after lb_spmv_host_x_wait(A), which blocks until every enqueued call's y is on the
  * host.  Pinned host buffers are required for the copies to overlap.  Products and summation order

@@ -1,6 +1,6 @@
 // lb_host.cu -- the host-buffer calls of liblb: lb_spmv_host (whole CSR uploaded per call),
 // lb_spmv_host_x (resident matrix, host x / y; LB_SPMV_CHUNKED overlaps the y download with the next
-// chunk's tiles) and lb_spmv_host_x_async / _wait (two staging slots, copies of neighbouring calls
+// chunk's tiles) and lb_spmv_host_x_async / _wait (three staging slots, copies of neighbouring calls
 // overlapped).  DESIGN.md 8.  C ABI in include/lb.h.
 #include "lb_internal.h"
 
@@ -57,7 +57,7 @@ void destroy_host_state(lb_csr_s* A) {
   if (h.mem) {
     if (h.h2d) cudaStreamSynchronize(h.h2d);
     if (h.d2h) cudaStreamSynchronize(h.d2h);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kHostSlots; ++i) {
       if (h.xready[i]) cudaEventDestroy(h.xready[i]);
       if (h.done[i]) cudaEventDestroy(h.done[i]);
       if (h.out[i]) cudaEventDestroy(h.out[i]);
@@ -160,13 +160,13 @@ lb_status_t lb_spmv_host_x_async(lb_csr_t A, lb_schedule_t sched, const float* h
   if (!h.mem) {
     const size_t xb = align256((size_t)A->cols * 4), yb = align256((size_t)A->rows * 4);
     void* p = nullptr;
-    if (cudaMalloc(&p, 2 * (xb + yb)) != cudaSuccess) {
+    if (cudaMalloc(&p, kHostSlots * (xb + yb)) != cudaSuccess) {
       cudaGetLastError();
       return fail(LB_ERR_OOM, "lb_spmv_host_x_async staging");
     }
     h.mem = p;
     char* b = static_cast<char*>(p);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kHostSlots; ++i) {
       h.x[i] = reinterpret_cast<float*>(b + i * (xb + yb));
       h.y[i] = reinterpret_cast<float*>(b + i * (xb + yb) + xb);
       LB_CUDA(cudaEventCreateWithFlags(&h.xready[i], cudaEventDisableTiming));
@@ -178,11 +178,11 @@ lb_status_t lb_spmv_host_x_async(lb_csr_t A, lb_schedule_t sched, const float* h
   }
   const int k = h.next;
   stream_t s = S(stream);
-  // x slot k is free once the SpMV of the call two back (same slot) has read it
+  // x slot k is free once the SpMV of the call kHostSlots back (same slot) has read it
   LB_CUDA(cudaStreamWaitEvent(h.h2d, h.done[k], 0));
   if (A->cols > 0) LB_CUDA(cudaMemcpyAsync(h.x[k], h_x, (size_t)A->cols * 4, cudaMemcpyHostToDevice, h.h2d));
   LB_CUDA(cudaEventRecord(h.xready[k], h.h2d));
-  // the SpMV waits for its x and for y slot k to have been copied out by the call two back
+  // the SpMV waits for its x and for y slot k to have been copied out by the call kHostSlots back
   LB_CUDA(cudaStreamWaitEvent(s, h.xready[k], 0));
   LB_CUDA(cudaStreamWaitEvent(s, h.out[k], 0));
   lb_status_t st = spmv_impl(A, sched, h.x[k], h.y[k], flags, s, nullptr);
@@ -191,7 +191,7 @@ lb_status_t lb_spmv_host_x_async(lb_csr_t A, lb_schedule_t sched, const float* h
   LB_CUDA(cudaStreamWaitEvent(h.d2h, h.done[k], 0));
   LB_CUDA(cudaMemcpyAsync(h_y, h.y[k], (size_t)A->rows * 4, cudaMemcpyDeviceToHost, h.d2h));
   LB_CUDA(cudaEventRecord(h.out[k], h.d2h));
-  h.next = k ^ 1;
+  h.next = (k + 1) % kHostSlots;
   return LB_OK;
 }
 

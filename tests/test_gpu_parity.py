@@ -97,6 +97,32 @@ def test_partition_random_every_diagonal():
         assert np.array_equal(M.partition(1).cpu().numpy(), oracle.partition(A.row_offsets, 1)), trial
 
 
+@pytest.mark.parametrize("extra", [-1, 0, 1])
+@pytest.mark.parametrize("shape", ["long_rows", "empty_runs"])
+def test_partition_both_search_kernels(shape, extra):
+    """The 16-lane group search (<= 32,768 boundaries) and the thread-per-boundary search (more) give
+    the brute-force coordinates on both sides of the switch: T + 1 = 32,768 - 1 .. + 1 at L = 64."""
+    L = 64
+    rng = np.random.default_rng(7 + extra)
+    target = (32768 - 1 + extra) * L - 1  # rows + nnz with T = ceil(total / L) = 32767 + extra
+    rows = 200_000 if shape == "long_rows" else 1_500_000
+    nnz = target - rows
+    if shape == "long_rows":  # a few very long rows among short ones
+        w = rng.pareto(1.2, rows) + 1e-3
+    else:  # long runs of empty rows between short ones
+        w = np.where(rng.random(rows) < 0.7, 0.0, rng.random(rows) + 0.1)
+    cnt = np.floor(w / w.sum() * nnz).astype(np.int64)
+    cnt[: nnz - int(cnt.sum())] += 1
+    off = np.zeros(rows + 1, np.int64)
+    np.cumsum(cnt, out=off[1:])
+    assert off[-1] == nnz
+    off_t = torch.from_numpy(off.astype(np.int32))
+    A = lbgen.Csr(rows, 64, off_t, torch.zeros(nnz, dtype=torch.int32), torch.ones(nnz))
+    M = lb.CsrMatrix.from_csr(A)
+    assert M.num_tiles(L) == 32767 + extra
+    assert np.array_equal(M.partition(L).cpu().numpy(), oracle.partition(off_t, L))
+
+
 # ---------------------------------------------------------------- SpMV parity
 
 @pytest.mark.parametrize("sched", SCHEDS)
@@ -314,7 +340,7 @@ def test_spmv_host_x_resident_matrix(sched):
 
 @pytest.mark.parametrize("sched", ["merge_path", "thread_mapped"])
 def test_spmv_host_x_async_pipeline(sched):
-    """lb_spmv_host_x_async: five independent x vectors enqueued back to back on the two staging slots
+    """lb_spmv_host_x_async: five independent x vectors enqueued back to back on the three staging slots
     (each call overlaps the previous calls' copies), one wait; every h_y equals the oracle bit for bit
     in integer mode, with and without the x-reuse plan, and a second batch reuses the slots."""
     A = lbgen.rmat(13, 16, 7, "int")
