@@ -278,6 +278,28 @@ def test_argument_errors():
         M.spmv(torch.ones(A.cols + 1, device="cuda"))
 
 
+def test_trace_phases_records_the_traced_calls():
+    """lb_csr_trace_phases / lb_csr_trace_read (bench.py times the tile kernel inside its timed region
+    with them): one (partition, main, fix-up) row per traced call up to the capacity, positive main
+    times, y unchanged by tracing, reset after a read, disabled by capacity 0."""
+    A = lbgen.rmat(14, 16, 4, "int")
+    x = lbgen.make_x(A.cols, "int", 2).cuda()
+    M = lb.CsrMatrix.from_csr(A)
+    y0 = M.spmv(x, schedule="merge_path", repartition=True).clone()
+    M.trace_phases(3)
+    for _ in range(5):
+        y = M.spmv(x, schedule="merge_path", repartition=True)
+    tr = M.trace_read()
+    assert tr.shape == (3, 3) and np.all(tr[:, 1] > 0) and np.all(tr >= 0)
+    assert torch.equal(y, y0)
+    assert M.trace_read().shape == (0, 3)  # reset by the read
+    M.spmv(x, schedule="thread_mapped")
+    assert M.trace_read().shape == (1, 3)  # capacity kept
+    M.trace_phases(0)
+    M.spmv(x, schedule="merge_path")
+    assert M.trace_read().shape == (0, 3)
+
+
 def test_deterministic_bitwise():
     A = lbgen.rmat(14, 16, 2, "float")
     x = lbgen.make_x(A.cols, "float", 8).cuda()
