@@ -172,7 +172,7 @@ struct TileKernel {
 };
 const TileKernel kTileKernels[kNumL] = {
     {"merge_stream_kernel<4,2,4>", stream_launch<4, 2, 4>},      // L = 504
-    {"merge_stream_kernel<8,4,2>", stream_launch<8, 4, 2>},      // L = 1016 (long / irregular rows)
+    {"merge_stream_kernel<16,4,1>", stream_launch<16, 4, 1>},    // L = 1016 (long / irregular rows)
     {"merge_rows_kernel<256,4>", rows_launch<256, 4>},           // L = 2040 (short rows: C2 stencil)
     {"merge_stream_kernel<4,12,4>", stream_launch<4, 12, 4>},    // L = 3064
     {"merge_wide_kernel<256,16,2>", wide_launch<256, 16, 2>},    // L = 4088
