@@ -80,3 +80,51 @@ def test_shape_limits_checked_before_any_access():
         st = L.lb_csr_create(rows, cols, nnz, fake, fake, fake, 0, None, ctypes.byref(h))
         assert st == lb.lb.LB_ERR_INVALID_ARG and not h, (rows, cols, nnz)
         assert "2^31" in lb.last_error() or "negative" in lb.last_error()
+
+
+# ---------------------------------------------------------------- host logic, property-based (no GPU)
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+
+@st.composite
+def _offsets(draw):
+    """Row offsets of a CSR with 0..300 rows of lengths 0..60 (many empty rows allowed)."""
+    lens = draw(st.lists(st.one_of(st.just(0), st.integers(0, 60)), min_size=0, max_size=300))
+    off = np.zeros(len(lens) + 1, np.int64)
+    np.cumsum(lens, out=off[1:])
+    return off.astype(np.int32)
+
+
+@settings(max_examples=150, deadline=None)
+@given(_offsets(), st.integers(1, 12))
+def test_shard_bounds_property(off, G):
+    """lb_shard_bounds equals the oracle's linear scan (b_g = min{r : off[r] >= ceil(g nnz / G)}) for any
+    offsets and rank count, including G > rows and nnz = 0; bounds are monotone from 0 to rows."""
+    got = lb.shard_bounds(off, G)
+    assert got.tolist() == oracle.shard_bounds(off, G).tolist()
+    assert got[0] == 0 and got[-1] == off.size - 1 and np.all(np.diff(got) >= 0)
+
+
+@settings(max_examples=150, deadline=None)
+@given(_offsets(), st.integers(1, 8), st.integers(1, 8), st.randoms(use_true_random=False))
+def test_exchange_schedule_property(off, G, K, rnd):
+    """lb_exchange_schedule over random bounds and random cut tables: the (chunk, root) broadcast ranges
+    tile [0, rows) exactly once, each inside its root's shard, in cut order; lb_padded_rows is the
+    largest shard."""
+    b = lb.shard_bounds(off, G)
+    rows = off.size - 1
+    cuts = np.zeros((G, K + 1), np.int64)
+    for k in range(G):
+        n = int(b[k + 1] - b[k])
+        inner = sorted(rnd.randint(0, n) for _ in range(K - 1))
+        cuts[k] = [0, *inner, n]
+    o, c = lb.exchange_schedule(b, cuts)
+    cover = np.zeros(rows, np.int64)
+    for ch in range(K):
+        for k in range(G):
+            s0, n = int(o[ch, k]), int(c[ch, k])
+            assert b[k] <= s0 and s0 + n <= b[k + 1]
+            assert s0 == b[k] + cuts[k, ch] and n == cuts[k, ch + 1] - cuts[k, ch]
+            cover[s0:s0 + n] += 1
+    assert np.all(cover == 1)
+    assert lb.padded_rows(b) == int(np.max(np.diff(b))) if G > 0 else 0
