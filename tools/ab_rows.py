@@ -1,5 +1,7 @@
-"""A/B of the short-row tile kernels at L = 2040 (LB_ROWS_VARIANT picks the kernel; one process per
-variant): median of 50 CUDA-graph replays of lb_spmv_ex(REPARTITION) per config; thread-mapped beside."""
+"""Short-row tile kernel at L = 2040 vs thread-mapped: median of 50 CUDA-graph replays of
+lb_spmv_ex(REPARTITION) per config, with per-phase times.  Round 2 ran it once per candidate kernel
+(selected by diagnostic environment switches that were removed with the losing candidates; the
+results are in profiles/r02_ab_short_rows_*.jsonl)."""
 import json, os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np
@@ -14,8 +16,8 @@ for cfg in cfgs:
     x = lbgen.x_for_config(cfg, A.cols, "float", device="cuda")
     M = lb.CsrMatrix.from_csr(A)
     y = torch.empty(A.rows, device="cuda")
-    M.set_items_per_tile(1016 if False else 2040)
-    out = {"config": cfg, "variant": os.environ.get("LB_SHORT_KERNEL", "0"), "kernel": M.kernel_name("merge_path")}
+    M.set_items_per_tile(2040)
+    out = {"config": cfg, "kernel": M.kernel_name("merge_path")}
     for sched in ("merge_path", "thread_mapped"):
         med, lo, hi = graph_median(lambda: M.spmv(x, y, sched, repartition=True), 50)
         ph = np.mean(np.array([M.phase_times(x, y, sched) for _ in range(20)]), axis=0)
